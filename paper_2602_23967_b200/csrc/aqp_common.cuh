@@ -1,0 +1,213 @@
+// aqp_common.cuh -- shared device/host helpers of libaqp.
+//
+// Arithmetic conventions (parity with the reference, anchorqp/_kernels/_core.pyx):
+//  * the whole library is compiled with --fmad=false: every a*b+c is a rounded
+//    multiply followed by a rounded add, exactly like the Cython kernels built
+//    by gcc -O2 for baseline x86-64 (no FMA contraction);
+//  * all reductions are deterministic: fixed per-thread order, fixed
+//    shuffle tree, fixed cross-warp / cross-block order (no float atomics), so
+//    a rerun reproduces every bit (reference tests/test_engine.py:307-314).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/aqp.h"
+
+namespace aqp {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+
+#define AQP_CUDA(call)                                                             \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return ::aqp::fail(AQP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + \
+                                        " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
+  } while (0)
+
+#define AQP_TRY(call)             \
+  do {                            \
+    int rc_ = (call);             \
+    if (rc_ != AQP_OK) return rc_; \
+  } while (0)
+
+// ---------------------------------------------------------------- constants
+constexpr int kThreads = 256;          // every kernel of the library uses 256-thread blocks
+constexpr int kWarps = kThreads / 32;
+constexpr int kTileNnz = 2048;         // nonzeros staged per SpMV row-block (16 KB + 8 KB smem)
+constexpr int kSegNnz = 8192;          // nonzeros per block for a split long row
+constexpr int kMaxRed = 16;            // max reduction slots of one kernel
+
+// ---------------------------------------------------------------- scalar helpers
+// Reference semantics: _clip in _core.pyx:21-26 (lo first, then hi; NaN passes through)
+__host__ __device__ __forceinline__ double clip(double v, double lo, double hi) {
+  if (v < lo) return lo;
+  if (v > hi) return hi;
+  return v;
+}
+
+// Python's built-in max(a, b) / min(a, b): keep a unless b compares greater / smaller
+__host__ __device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
+__host__ __device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
+
+// numpy.max over nonnegative values with NaN propagation (np.abs(v).max())
+__device__ __forceinline__ double nanmax(double a, double b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return b > a ? b : a;
+}
+
+// cone projection, _core.pyx:95-115 (ZERO, NONNEG, NONPOS, FREE)
+__device__ __forceinline__ double cone_proj(double v, int8_t code) {
+  if (code == AQP_ZERO) return 0.0;
+  if (code == AQP_NONNEG) return v > 0.0 ? v : 0.0;
+  if (code == AQP_NONPOS) return v < 0.0 ? v : 0.0;
+  return v;
+}
+
+// support_p term split (model.py:57-71): positive part against upper bound,
+// negative part against lower bound; flag when a nonzero part meets an
+// infinite bound of matching sign.
+struct SupportAcc {
+  double pos, neg, bad;
+};
+__device__ __forceinline__ void support_add(double z, double lo, double hi, double &pos, double &neg,
+                                            double &bad) {
+  if (z > 0.0) {
+    if (isinf(hi)) bad = 1.0; else pos += hi * z;
+  } else if (z < 0.0) {
+    if (isinf(lo)) bad = 1.0; else neg += lo * z;
+  }
+}
+
+// ---------------------------------------------------------------- deterministic reductions
+template <int NS, int NM>
+struct RedVals {
+  double s[NS > 0 ? NS : 1];
+  double m[NM > 0 ? NM : 1];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) s[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) m[i] = 0.0;
+  }
+};
+
+// Block reduction of NS sums and NM NaN-propagating maxes; result valid in
+// thread 0.  Fixed xor-shuffle tree inside warps, then warp 0 folds the
+// per-warp values in warp order.
+template <int NS, int NM>
+__device__ __forceinline__ void block_reduce(RedVals<NS, NM> &v, double *smem /* kWarps*(NS+NM) */) {
+  constexpr int NT = NS + NM;
+  if constexpr (NT == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) v.s[i] += __shfl_xor_sync(0xffffffffu, v.s[i], off);
+#pragma unroll
+    for (int i = 0; i < NM; ++i) v.m[i] = nanmax(v.m[i], __shfl_xor_sync(0xffffffffu, v.m[i], off));
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) smem[warp * NT + i] = v.s[i];
+#pragma unroll
+    for (int i = 0; i < NM; ++i) smem[warp * NT + NS + i] = v.m[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      double a = smem[i];
+      for (int w = 1; w < kWarps; ++w) a += smem[w * NT + i];
+      v.s[i] = a;
+    }
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+      double a = smem[NS + i];
+      for (int w = 1; w < kWarps; ++w) a = nanmax(a, smem[w * NT + NS + i]);
+      v.m[i] = a;
+    }
+  }
+  __syncthreads();
+}
+
+// Grid-level epilogue shared by every reducing kernel: each block publishes
+// its partials; the last block to arrive (integer atomic ticket -- the
+// ticket order does not affect the arithmetic) folds all partials in block
+// order and returns true in thread 0 with the grid totals in `v`.
+struct GridRed {
+  double *partials;     // >= gridDim.x * (NS+NM) doubles
+  unsigned int *ticket;  // zero between launches (reset by the last block)
+};
+
+template <int NS, int NM>
+__device__ __forceinline__ bool grid_reduce(RedVals<NS, NM> &v, GridRed g, double *smem) {
+  constexpr int NT = NS + NM;
+  __shared__ bool last;
+  if constexpr (NT > 0) {
+    block_reduce<NS, NM>(v, smem);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int i = 0; i < NS; ++i) g.partials[(size_t)blockIdx.x * NT + i] = v.s[i];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) g.partials[(size_t)blockIdx.x * NT + NS + i] = v.m[i];
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(g.ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  if constexpr (NT > 0) {
+    // thread t folds blocks t, t+256, ... sequentially, then the fixed tree
+    RedVals<NS, NM> a;
+    a.zero();
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += kThreads) {
+      const double *p = g.partials + (size_t)b * NT;
+#pragma unroll
+      for (int i = 0; i < NS; ++i) a.s[i] += __ldcg(p + i);
+#pragma unroll
+      for (int i = 0; i < NM; ++i) a.m[i] = nanmax(a.m[i], __ldcg(p + NS + i));
+    }
+    block_reduce<NS, NM>(a, smem);
+    v = a;
+  }
+  if (threadIdx.x == 0) *g.ticket = 0u;
+  return threadIdx.x == 0;
+}
+
+// ---------------------------------------------------------------- SpMV work partition
+// One block per item.  THREAD: rows [row0,row1) whose nonzeros [k0,k1) fit
+// one smem tile, one thread per row, row sum sequential in column order
+// (bitwise the Cython order).  WARP: same tile, one warp per row (used when
+// rows are long enough that a sequential chain would be latency bound).
+// LONG: segment `seg` of `nseg` of one row longer than a tile.
+enum : int { kItemThread = 0, kItemWarp = 1, kItemLong = 2 };
+
+struct __align__(16) PlanItem {
+  int row0, row1, k0, k1;
+  int kind, seg, nseg, segbase;
+};
+
+// device CSR with int32 indices plus its work plan
+struct DevCsr {
+  int rows = 0, cols = 0;
+  int64_t nnz = 0;
+  const int *ptr = nullptr;
+  const int *idx = nullptr;
+  const double *val = nullptr;
+  const PlanItem *plan = nullptr;
+  int nitems = 0;
+  int nlongseg = 0;
+  double *seg_part = nullptr;          // 2 * nlongseg doubles
+  unsigned int *seg_ticket = nullptr;  // nlongseg counters
+};
+
+}  // namespace aqp

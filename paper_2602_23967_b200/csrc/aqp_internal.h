@@ -1,0 +1,58 @@
+// aqp_internal.h -- library-private structs shared by the .cu files.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "aqp_common.cuh"
+
+// bump allocator over a caller-provided workspace; with base == nullptr it
+// only measures (the "sizes" dry run uses the very same layout code)
+namespace aqp {
+struct Bump {
+  void *base = nullptr;
+  size_t cap = 0;
+  size_t used = 0;
+  bool overflow = false;
+  void *take(size_t bytes);
+};
+
+struct CsrStore {
+  int *ptr = nullptr;
+  int *idx = nullptr;
+  double *val = nullptr;
+  PlanItem *plan = nullptr;
+  int64_t plan_cap = 0;
+  double *seg_part = nullptr;
+  unsigned *seg_ticket = nullptr;
+  int64_t seg_cap = 0;
+};
+
+void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz);
+int upload_csr(aqp_ctx *ctx, CsrStore &s, DevCsr &M, int64_t rows, int64_t cols, const int64_t *d_ptr,
+               const int64_t *d_idx, const double *d_val, int64_t nnz, const int64_t *host_ptr, bool strict,
+               int *d_bad);
+int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool strict, Bump &scratch);
+int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool strict, Bump &scratch,
+                   int64_t *nfull_out);
+size_t transpose_scratch_bytes(int64_t nnz, int64_t cols);
+size_t symmetrize_scratch_bytes(int64_t nnz, int64_t n);
+}  // namespace aqp
+
+struct aqp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+};
+
+struct aqp_problem {
+  aqp_ctx *ctx = nullptr;
+  int64_t n = 0, m = 0;
+  int quad_kind = 0;
+  aqp::CsrStore sA, sAt, sQ, sR, sRt;
+  aqp::DevCsr A, At, Q, R, Rt;
+  int64_t q_full_nnz = 0;
+  double *c = nullptr, *vlo = nullptr, *vhi = nullptr, *qd = nullptr, *clo = nullptr, *chi = nullptr;
+  int8_t *cone_r = nullptr, *recc_x = nullptr, *cone_y = nullptr, *recc_s = nullptr;
+  int *bad = nullptr;
+  aqp_problem_info info{};
+};

@@ -1,0 +1,577 @@
+// aqp_problem.cu -- context, device problem upload and the SpMV work planner.
+//
+// Device layout of a problem (all in one caller-provided persistent workspace):
+//   A   : m x n CSR, int32 ptr/idx, f64 val                 (reference linalg.py:28-112)
+//   A'  : n x m CSR built on the device by a STABLE radix sort of A's entries
+//         by column -- entries of a column keep ascending row order, so the
+//         row-sequential A' product reproduces the Cython scatter order of
+//         _core.pyx:45-59 bit for bit, with no atomics.
+//   Q   : n x n full symmetric CSR expanded from the upper triangle
+//         (linalg.py:177-227); each row is [mirrored lower part | stored upper
+//         part] in ascending column order, again via one stable sort.
+//   R, R' (low-rank kind): k x n CSR and its transpose (linalg.py:230-266).
+//   c, l_v, u_v, l_c, u_c; int8 cone codes (model.py:85-112) built on device.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "aqp_common.cuh"
+#include "aqp_internal.h"
+
+namespace aqp {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string &msg) { g_last_error = msg; }
+int fail(int code, const std::string &msg) {
+  set_error(msg);
+  return code;
+}
+
+// ---------------------------------------------------------------- bump allocator
+void *Bump::take(size_t bytes) {
+  size_t off = (used + 255) & ~size_t(255);
+  used = off + bytes;
+  if (base == nullptr) return nullptr;
+  if (used > cap) {
+    overflow = true;
+    return nullptr;
+  }
+  return static_cast<char *>(base) + off;
+}
+
+// ---------------------------------------------------------------- planner
+template <class P>
+static std::vector<PlanItem> plan_rows(const P *ptr, int64_t rows, bool strict, int *nlongseg) {
+  std::vector<PlanItem> items;
+  int segs = 0;
+  int64_t i = 0;
+  while (i < rows) {
+    const int64_t len = (int64_t)(ptr[i + 1] - ptr[i]);
+    if (len > kTileNnz) {
+      const int nseg = (int)((len + kSegNnz - 1) / kSegNnz);
+      for (int s = 0; s < nseg; ++s) {
+        PlanItem it{};
+        it.row0 = (int)i;
+        it.row1 = (int)i + 1;
+        it.k0 = (int)(ptr[i] + (int64_t)s * kSegNnz);
+        it.k1 = (int)std::min<int64_t>(ptr[i] + (int64_t)(s + 1) * kSegNnz, ptr[i + 1]);
+        it.kind = kItemLong;
+        it.seg = s;
+        it.nseg = nseg;
+        it.segbase = segs;
+        items.push_back(it);
+      }
+      segs += nseg;
+      ++i;
+      continue;
+    }
+    const int64_t start = i;
+    int64_t nnz = 0;
+    while (i < rows && i - start < kThreads) {
+      const int64_t l = (int64_t)(ptr[i + 1] - ptr[i]);
+      if (l > kTileNnz || nnz + l > kTileNnz) break;
+      nnz += l;
+      ++i;
+    }
+    PlanItem it{};
+    it.row0 = (int)start;
+    it.row1 = (int)i;
+    it.k0 = (int)ptr[start];
+    it.k1 = (int)ptr[i];
+    // rows averaging more than ~24 nonzeros: a sequential per-thread chain
+    // would dominate; switch to one warp per row (tree order, deterministic)
+    it.kind = (!strict && nnz > 24 * (i - start)) ? kItemWarp : kItemThread;
+    items.push_back(it);
+  }
+  if (items.empty()) {  // zero rows: one empty item so fused finalizers still run
+    PlanItem it{};
+    it.kind = kItemThread;
+    items.push_back(it);
+  }
+  *nlongseg = segs;
+  return items;
+}
+
+int64_t plan_capacity(int64_t rows, int64_t nnz) {
+  return rows / 128 + 2 * (nnz / kTileNnz) + nnz / kSegNnz + 8;
+}
+
+// ---------------------------------------------------------------- setup kernels
+__global__ void k_i64_to_i32(const int64_t *__restrict__ in, int *__restrict__ out, int64_t n,
+                             int64_t limit, int *bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = in[i];
+    if (v < 0 || v > limit) *bad = 1;
+    out[i] = (int)v;
+  }
+}
+
+__global__ void k_row_ids(const int *__restrict__ ptr, int rows, int *__restrict__ rid) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    for (int k = ptr[r]; k < ptr[r + 1]; ++k) rid[k] = r;
+}
+
+__global__ void k_iota(int *out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int)i;
+}
+
+__global__ void k_hist(const int *__restrict__ keys, int64_t n, int *counts) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(counts + keys[i], 1);  // integer counts: order-independent
+}
+
+// transpose gather: out entry p comes from source entry src[p]
+__global__ void k_gather_t(const int *__restrict__ src, const int *__restrict__ rid,
+                           const double *__restrict__ val, int64_t n, int *__restrict__ out_idx,
+                           double *__restrict__ out_val) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int k = src[p];
+    out_idx[p] = rid[k];
+    out_val[p] = val[k];
+  }
+}
+
+// full-symmetric expansion: combined entry list is
+//   [0, nnz)      mirrored copies (row = col_k, col = row_k), diagonal -> sentinel row n
+//   [nnz, 2nnz)   the stored upper entries (row = row_k, col = col_k)
+__global__ void k_sym_keys(const int *__restrict__ rid, const int *__restrict__ col, int64_t nnz, int n,
+                           int *__restrict__ keys) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rid[k], c = col[k];
+    keys[k] = (c == r) ? n : c;
+    keys[nnz + k] = r;
+  }
+}
+
+__global__ void k_sym_gather(const int *__restrict__ src, const int *__restrict__ rid,
+                             const int *__restrict__ col, const double *__restrict__ val, int64_t nnz,
+                             int64_t nfull, int *__restrict__ out_idx, double *__restrict__ out_val) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nfull; p += (int64_t)gridDim.x * blockDim.x) {
+    const int s = src[p];
+    if (s < nnz) {  // mirrored: column is the source row
+      out_idx[p] = rid[s];
+      out_val[p] = val[s];
+    } else {
+      out_idx[p] = col[s - nnz];
+      out_val[p] = val[s - nnz];
+    }
+  }
+}
+
+// cone tables of model.py:85-112 indexed by (lower finite)*2 + (upper finite)
+__global__ void k_cones(const double *__restrict__ lo, const double *__restrict__ hi, int64_t n,
+                        int8_t *__restrict__ dual, int8_t *__restrict__ recc, int dual_is_y) {
+  // dual_y: (F,F)->ZERO (F,T)->NONNEG (T,F)->NONPOS (T,T)->FREE
+  // dual_r: (F,F)->ZERO (F,T)->NONPOS (T,F)->NONNEG (T,T)->FREE
+  // recession: (F,F)->FREE (F,T)->NONPOS (T,F)->NONNEG (T,T)->ZERO
+  const int8_t ty[4] = {AQP_ZERO, AQP_NONNEG, AQP_NONPOS, AQP_FREE};
+  const int8_t tr[4] = {AQP_ZERO, AQP_NONPOS, AQP_NONNEG, AQP_FREE};
+  const int8_t tc[4] = {AQP_FREE, AQP_NONPOS, AQP_NONNEG, AQP_ZERO};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (isfinite(lo[i]) ? 2 : 0) + (isfinite(hi[i]) ? 1 : 0);
+    dual[i] = dual_is_y ? ty[p] : tr[p];
+    recc[i] = tc[p];
+  }
+}
+
+static inline int setup_grid(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)b;
+}
+
+// ---------------------------------------------------------------- CSR upload / transpose
+static size_t sort_temp_bytes(int64_t n_items) {
+  size_t a = 0, b = 0;
+  if (n_items <= 0) n_items = 1;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (const int *)nullptr, (int *)nullptr, (const int *)nullptr,
+                                  (int *)nullptr, (int)n_items);
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (const int *)nullptr, (int *)nullptr, (int)n_items + 1);
+  return std::max(a, b);
+}
+
+static int to_i32(const int64_t *in, int *out, int64_t n, int64_t limit, int *d_bad, cudaStream_t st) {
+  if (n == 0) return AQP_OK;
+  k_i64_to_i32<<<setup_grid(n), 256, 0, st>>>(in, out, n, limit, d_bad);
+  AQP_CUDA(cudaGetLastError());
+  return AQP_OK;
+}
+
+// ptr: (rows+1) counts -> exclusive scan; keys sorted stably
+static int counts_to_ptr(int *counts, int rows, int *ptr_out, void *tmp, size_t tmp_bytes, cudaStream_t st) {
+  size_t need = tmp_bytes;
+  AQP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, counts, ptr_out, rows + 1, st));
+  return AQP_OK;
+}
+
+int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *host_ptr64, bool strict,
+                PlanItem *plan_dev, int64_t plan_cap, double *seg_part, unsigned *seg_ticket,
+                int64_t seg_cap) {
+  int nlong = 0;
+  std::vector<PlanItem> items = host_ptr64 ? plan_rows(host_ptr64, M.rows, strict, &nlong)
+                                           : plan_rows(host_ptr32, M.rows, strict, &nlong);
+  if ((int64_t)items.size() > plan_cap) return fail(AQP_ENOMEM, "plan capacity exceeded");
+  if (nlong > seg_cap) return fail(AQP_ENOMEM, "segment capacity exceeded");
+  AQP_CUDA(cudaMemcpyAsync(plan_dev, items.data(), items.size() * sizeof(PlanItem), cudaMemcpyHostToDevice,
+                           ctx->stream));
+  AQP_CUDA(cudaStreamSynchronize(ctx->stream));  // `items` is pageable and local
+  M.plan = plan_dev;
+  M.nitems = (int)items.size();
+  M.nlongseg = nlong;
+  M.seg_part = seg_part;
+  M.seg_ticket = seg_ticket;
+  return AQP_OK;
+}
+
+// Persistent storage of one device CSR with its plan.
+void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz) {
+  s.ptr = (int *)b.take((rows + 1) * sizeof(int));
+  s.idx = (int *)b.take(std::max<int64_t>(nnz, 1) * sizeof(int));
+  s.val = (double *)b.take(std::max<int64_t>(nnz, 1) * sizeof(double));
+  s.plan_cap = plan_capacity(rows, nnz);
+  s.plan = (PlanItem *)b.take(s.plan_cap * sizeof(PlanItem));
+  s.seg_cap = nnz / kSegNnz + 2;
+  s.seg_part = (double *)b.take(2 * s.seg_cap * sizeof(double));
+  s.seg_ticket = (unsigned *)b.take(s.seg_cap * sizeof(unsigned));
+}
+
+// Upload an int64 CSR (device pointers) into int32 storage and plan it.
+int upload_csr(aqp_ctx *ctx, CsrStore &s, DevCsr &M, int64_t rows, int64_t cols, const int64_t *d_ptr,
+               const int64_t *d_idx, const double *d_val, int64_t nnz, const int64_t *host_ptr, bool strict,
+               int *d_bad) {
+  cudaStream_t st = ctx->stream;
+  AQP_TRY(to_i32(d_ptr, s.ptr, rows + 1, INT32_MAX, d_bad, st));
+  AQP_TRY(to_i32(d_idx, s.idx, nnz, cols - 1, d_bad, st));
+  if (nnz) AQP_CUDA(cudaMemcpyAsync(s.val, d_val, nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  AQP_CUDA(cudaMemsetAsync(s.seg_ticket, 0, s.seg_cap * sizeof(unsigned), st));
+  M.rows = (int)rows;
+  M.cols = (int)cols;
+  M.nnz = nnz;
+  M.ptr = s.ptr;
+  M.idx = s.idx;
+  M.val = s.val;
+  return finish_plan(ctx, M, nullptr, host_ptr, strict, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap);
+}
+
+// Transpose of an uploaded CSR (src) into storage t (rows = src.cols).
+// Scratch: rid(nnz) keys(nnz) keys2(nnz) vals(nnz) vals2(nnz) counts(cols+1) + cub.
+int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool strict, Bump &scratch) {
+  cudaStream_t st = ctx->stream;
+  const int64_t nnz = src.nnz;
+  const int rows_t = src.cols;
+  scratch.used = 0;
+  int *rid = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
+  int *keys2 = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
+  int *vals = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
+  int *vals2 = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
+  int *counts = (int *)scratch.take((int64_t)(rows_t + 1) * 4);
+  size_t tb = sort_temp_bytes(std::max<int64_t>(nnz, rows_t + 1));
+  void *tmp = scratch.take(tb);
+  if (scratch.overflow) return fail(AQP_ENOMEM, "transpose scratch too small");
+  AQP_CUDA(cudaMemsetAsync(counts, 0, (rows_t + 1) * sizeof(int), st));
+  if (nnz) {
+    k_row_ids<<<setup_grid(src.rows), 256, 0, st>>>(src.ptr, src.rows, rid);
+    k_iota<<<setup_grid(nnz), 256, 0, st>>>(vals, nnz);
+    k_hist<<<setup_grid(nnz), 256, 0, st>>>(src.idx, nnz, counts);
+    AQP_CUDA(cudaGetLastError());
+    int end_bit = 1;
+    while ((1LL << end_bit) <= (int64_t)rows_t) ++end_bit;
+    size_t need = tb;
+    AQP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, src.idx, keys2, vals, vals2, (int)nnz, 0, end_bit, st));
+    k_gather_t<<<setup_grid(nnz), 256, 0, st>>>(vals2, rid, src.val, nnz, t.idx, t.val);
+    AQP_CUDA(cudaGetLastError());
+  }
+  AQP_TRY(counts_to_ptr(counts, rows_t, t.ptr, tmp, tb, st));
+  AQP_CUDA(cudaMemsetAsync(t.seg_ticket, 0, t.seg_cap * sizeof(unsigned), st));
+  T.rows = rows_t;
+  T.cols = src.rows;
+  T.nnz = nnz;
+  T.ptr = t.ptr;
+  T.idx = t.idx;
+  T.val = t.val;
+  std::vector<int> hptr(rows_t + 1);
+  AQP_CUDA(cudaMemcpyAsync(hptr.data(), t.ptr, (rows_t + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  return finish_plan(ctx, T, hptr.data(), nullptr, strict, t.plan, t.plan_cap, t.seg_part, t.seg_ticket, t.seg_cap);
+}
+
+// Full symmetric expansion of an uploaded upper-triangle CSR U (n x n).
+int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool strict, Bump &scratch,
+                   int64_t *nfull_out) {
+  cudaStream_t st = ctx->stream;
+  const int64_t nnz = U.nnz;
+  const int n = U.rows;
+  const int64_t n2 = 2 * nnz;
+  scratch.used = 0;
+  int *rid = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
+  int *keys = (int *)scratch.take(std::max<int64_t>(n2, 1) * 4);
+  int *keys2 = (int *)scratch.take(std::max<int64_t>(n2, 1) * 4);
+  int *vals = (int *)scratch.take(std::max<int64_t>(n2, 1) * 4);
+  int *vals2 = (int *)scratch.take(std::max<int64_t>(n2, 1) * 4);
+  int *counts = (int *)scratch.take((int64_t)(n + 2) * 4);
+  size_t tb = sort_temp_bytes(std::max<int64_t>(n2, n + 2));
+  void *tmp = scratch.take(tb);
+  if (scratch.overflow) return fail(AQP_ENOMEM, "symmetrize scratch too small");
+  AQP_CUDA(cudaMemsetAsync(counts, 0, (n + 2) * sizeof(int), st));
+  int64_t nfull = 0;
+  if (nnz) {
+    k_row_ids<<<setup_grid(n), 256, 0, st>>>(U.ptr, n, rid);
+    k_sym_keys<<<setup_grid(nnz), 256, 0, st>>>(rid, U.idx, nnz, n, keys);
+    k_iota<<<setup_grid(n2), 256, 0, st>>>(vals, n2);
+    k_hist<<<setup_grid(n2), 256, 0, st>>>(keys, n2, counts);  // counts[n] = #diagonal sentinels
+    AQP_CUDA(cudaGetLastError());
+    int end_bit = 1;
+    while ((1LL << end_bit) <= (int64_t)n) ++end_bit;
+    size_t need = tb;
+    AQP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, keys, keys2, vals, vals2, (int)n2, 0, end_bit, st));
+    int ndiag = 0;
+    AQP_CUDA(cudaMemcpyAsync(&ndiag, counts + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    AQP_CUDA(cudaStreamSynchronize(st));
+    nfull = n2 - ndiag;
+    k_sym_gather<<<setup_grid(nfull), 256, 0, st>>>(vals2, rid, U.idx, U.val, nnz, nfull, f.idx, f.val);
+    AQP_CUDA(cudaGetLastError());
+  }
+  AQP_CUDA(cudaMemsetAsync(counts + n, 0, sizeof(int), st));
+  AQP_TRY(counts_to_ptr(counts, n, f.ptr, tmp, tb, st));
+  AQP_CUDA(cudaMemsetAsync(f.seg_ticket, 0, f.seg_cap * sizeof(unsigned), st));
+  F.rows = n;
+  F.cols = n;
+  F.nnz = nfull;
+  F.ptr = f.ptr;
+  F.idx = f.idx;
+  F.val = f.val;
+  *nfull_out = nfull;
+  std::vector<int> hptr(n + 1);
+  AQP_CUDA(cudaMemcpyAsync(hptr.data(), f.ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  return finish_plan(ctx, F, hptr.data(), nullptr, strict, f.plan, f.plan_cap, f.seg_part, f.seg_ticket, f.seg_cap);
+}
+
+size_t transpose_scratch_bytes(int64_t nnz, int64_t cols) {
+  Bump b;
+  b.take(std::max<int64_t>(nnz, 1) * 4);
+  b.take(std::max<int64_t>(nnz, 1) * 4);
+  b.take(std::max<int64_t>(nnz, 1) * 4);
+  b.take(std::max<int64_t>(nnz, 1) * 4);
+  b.take((cols + 1) * 4);
+  b.take(sort_temp_bytes(std::max<int64_t>(nnz, cols + 1)));
+  return b.used + 256;
+}
+
+size_t symmetrize_scratch_bytes(int64_t nnz, int64_t n) {
+  Bump b;
+  b.take(std::max<int64_t>(nnz, 1) * 4);
+  for (int i = 0; i < 4; ++i) b.take(std::max<int64_t>(2 * nnz, 1) * 4);
+  b.take((n + 2) * 4);
+  b.take(sort_temp_bytes(std::max<int64_t>(2 * nnz, n + 2)));
+  return b.used + 256;
+}
+
+int build_cones(aqp_ctx *ctx, const double *lo, const double *hi, int64_t n, int8_t *dual, int8_t *recc,
+                int is_y) {
+  if (n == 0) return AQP_OK;
+  k_cones<<<setup_grid(n), 256, 0, ctx->stream>>>(lo, hi, n, dual, recc, is_y);
+  AQP_CUDA(cudaGetLastError());
+  return AQP_OK;
+}
+
+}  // namespace aqp
+
+using namespace aqp;
+
+// ====================================================================== C ABI
+extern "C" {
+
+int aqp_abi_version(void) { return AQP_ABI_VERSION; }
+const char *aqp_last_error(void) { return g_last_error.c_str(); }
+
+int aqp_ctx_create(int device, void *stream, aqp_ctx **out) {
+  if (!out) return fail(AQP_EINVAL, "out is NULL");
+  AQP_CUDA(cudaSetDevice(device));
+  aqp_ctx *c = new aqp_ctx();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(stream);
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  *out = c;
+  return AQP_OK;
+}
+
+int aqp_ctx_destroy(aqp_ctx *ctx) {
+  delete ctx;
+  return AQP_OK;
+}
+
+static int check_desc(const aqp_problem_desc *d) {
+  if (!d) return fail(AQP_EINVAL, "desc is NULL");
+  if (d->n < 0 || d->m < 0) return fail(AQP_EINVAL, "negative dimension");
+  if (d->n >= INT32_MAX || d->m >= INT32_MAX || d->a_nnz >= INT32_MAX / 2 || d->q_nnz >= INT32_MAX / 4 ||
+      d->r_nnz >= INT32_MAX / 2 || d->r_rows >= INT32_MAX)
+    return fail(AQP_ERANGE, "instance exceeds int32 device indexing");
+  if (d->quad_kind < AQP_QUAD_DIAGONAL || d->quad_kind > AQP_QUAD_SPARSE_LOW_RANK)
+    return fail(AQP_EINVAL, "unknown quad kind");
+  return AQP_OK;
+}
+
+static void layout_problem(Bump &b, const aqp_problem_desc *d, aqp_problem *p) {
+  const int64_t n = d->n, m = d->m;
+  layout_csr(b, p->sA, m, d->a_nnz);
+  layout_csr(b, p->sAt, n, d->a_nnz);
+  if (d->quad_kind != AQP_QUAD_DIAGONAL) layout_csr(b, p->sQ, n, 2 * d->q_nnz);
+  if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
+    layout_csr(b, p->sR, d->r_rows, d->r_nnz);
+    layout_csr(b, p->sRt, n, d->r_nnz);
+  }
+  p->c = (double *)b.take(std::max<int64_t>(n, 1) * 8);
+  p->vlo = (double *)b.take(std::max<int64_t>(n, 1) * 8);
+  p->vhi = (double *)b.take(std::max<int64_t>(n, 1) * 8);
+  p->qd = (double *)b.take(std::max<int64_t>(n, 1) * 8);
+  p->clo = (double *)b.take(std::max<int64_t>(m, 1) * 8);
+  p->chi = (double *)b.take(std::max<int64_t>(m, 1) * 8);
+  p->cone_r = (int8_t *)b.take(std::max<int64_t>(n, 1));
+  p->recc_x = (int8_t *)b.take(std::max<int64_t>(n, 1));
+  p->cone_y = (int8_t *)b.take(std::max<int64_t>(m, 1));
+  p->recc_s = (int8_t *)b.take(std::max<int64_t>(m, 1));
+  p->bad = (int *)b.take(64);
+}
+
+int aqp_problem_sizes(const aqp_problem_desc *d, size_t *persistent_bytes, size_t *scratch_bytes) {
+  AQP_TRY(check_desc(d));
+  aqp_problem tmp;
+  Bump b;
+  layout_problem(b, d, &tmp);
+  size_t sc = transpose_scratch_bytes(d->a_nnz, d->n);
+  if (d->quad_kind != AQP_QUAD_DIAGONAL) {
+    // the int32 upper triangle sits at the front of the scratch during the expansion
+    const size_t up = (size_t)(d->n + 1) * 4 + (size_t)std::max<int64_t>(d->q_nnz, 1) * 12 + 1024;
+    sc = std::max(sc, up + symmetrize_scratch_bytes(d->q_nnz, d->n));
+  }
+  if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) sc = std::max(sc, transpose_scratch_bytes(d->r_nnz, d->n));
+  if (persistent_bytes) *persistent_bytes = b.used + 256;
+  if (scratch_bytes) *scratch_bytes = sc;
+  return AQP_OK;
+}
+
+int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *host_a_indptr,
+                       const int64_t *host_q_indptr, const int64_t *host_r_indptr, void *persistent,
+                       size_t persistent_bytes, void *scratch, size_t scratch_bytes, aqp_problem **out) {
+  (void)host_q_indptr;
+  AQP_TRY(check_desc(d));
+  if (!ctx || !out || !persistent || !host_a_indptr) return fail(AQP_EINVAL, "NULL argument");
+  if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && !host_r_indptr) return fail(AQP_EINVAL, "R indptr missing");
+  AQP_CUDA(cudaSetDevice(ctx->device));
+  aqp_problem *p = new aqp_problem();
+  p->ctx = ctx;
+  p->n = d->n;
+  p->m = d->m;
+  p->quad_kind = d->quad_kind;
+  Bump b;
+  b.base = persistent;
+  b.cap = persistent_bytes;
+  layout_problem(b, d, p);
+  if (b.overflow) {
+    delete p;
+    return fail(AQP_ENOMEM, "persistent workspace too small");
+  }
+  Bump sc;
+  sc.base = scratch;
+  sc.cap = scratch_bytes;
+  cudaStream_t st = ctx->stream;
+  int rc = AQP_OK;
+  auto cleanup = [&](int code) {
+    delete p;
+    return code;
+  };
+  AQP_CUDA(cudaMemsetAsync(p->bad, 0, 64, st));
+  rc = upload_csr(ctx, p->sA, p->A, d->m, d->n, d->a_indptr, d->a_indices, d->a_data, d->a_nnz, host_a_indptr,
+                  false, p->bad);
+  if (rc) return cleanup(rc);
+  rc = transpose_csr(ctx, p->A, p->sAt, p->At, false, sc);
+  if (rc) return cleanup(rc);
+  p->q_full_nnz = 0;
+  const int64_t n = d->n, m = d->m;
+  if (d->quad_kind == AQP_QUAD_DIAGONAL) {
+    if (n) AQP_CUDA(cudaMemcpyAsync(p->qd, d->q_values, n * 8, cudaMemcpyDeviceToDevice, st));
+  } else {
+    // upload the upper triangle into the A' storage temporarily? no: into sQ's
+    // tail is unsafe; use the scratch-free path: upload to sQ, then expand via
+    // scratch copies of the upper arrays
+    DevCsr U;
+    CsrStore su;
+    Bump ub;  // the upper CSR lives in the first part of the scratch workspace
+    ub.base = scratch;
+    ub.cap = scratch_bytes;
+    su.ptr = (int *)ub.take((n + 1) * 4);
+    su.idx = (int *)ub.take(std::max<int64_t>(d->q_nnz, 1) * 4);
+    su.val = (double *)ub.take(std::max<int64_t>(d->q_nnz, 1) * 8);
+    if (ub.overflow) return cleanup(fail(AQP_ENOMEM, "scratch too small for Q upload"));
+    rc = to_i32(d->q_indptr, su.ptr, n + 1, INT32_MAX, p->bad, st);
+    if (!rc) rc = to_i32(d->q_indices, su.idx, d->q_nnz, n - 1, p->bad, st);
+    if (rc) return cleanup(rc);
+    if (d->q_nnz) AQP_CUDA(cudaMemcpyAsync(su.val, d->q_data, d->q_nnz * 8, cudaMemcpyDeviceToDevice, st));
+    U.rows = (int)n;
+    U.cols = (int)n;
+    U.nnz = d->q_nnz;
+    U.ptr = su.ptr;
+    U.idx = su.idx;
+    U.val = su.val;
+    Bump rest;
+    rest.base = static_cast<char *>(scratch) + ((ub.used + 255) & ~size_t(255));
+    rest.cap = scratch_bytes - ((ub.used + 255) & ~size_t(255));
+    rc = symmetrize_csr(ctx, U, p->sQ, p->Q, false, rest, &p->q_full_nnz);
+    if (rc) return cleanup(rc);
+    if (n) AQP_CUDA(cudaMemcpyAsync(p->qd, d->q_diag, n * 8, cudaMemcpyDeviceToDevice, st));
+    if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
+      rc = upload_csr(ctx, p->sR, p->R, d->r_rows, d->n, d->r_indptr, d->r_indices, d->r_data, d->r_nnz,
+                      host_r_indptr, false, p->bad);
+      if (!rc) rc = transpose_csr(ctx, p->R, p->sRt, p->Rt, false, sc);
+      if (rc) return cleanup(rc);
+    }
+  }
+  if (n) {
+    AQP_CUDA(cudaMemcpyAsync(p->c, d->cost, n * 8, cudaMemcpyDeviceToDevice, st));
+    AQP_CUDA(cudaMemcpyAsync(p->vlo, d->var_lo, n * 8, cudaMemcpyDeviceToDevice, st));
+    AQP_CUDA(cudaMemcpyAsync(p->vhi, d->var_hi, n * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  if (m) {
+    AQP_CUDA(cudaMemcpyAsync(p->clo, d->con_lo, m * 8, cudaMemcpyDeviceToDevice, st));
+    AQP_CUDA(cudaMemcpyAsync(p->chi, d->con_hi, m * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  rc = build_cones(ctx, p->vlo, p->vhi, n, p->cone_r, p->recc_x, 0);
+  if (!rc) rc = build_cones(ctx, p->clo, p->chi, m, p->cone_y, p->recc_s, 1);
+  if (rc) return cleanup(rc);
+  int bad = 0;
+  AQP_CUDA(cudaMemcpyAsync(&bad, p->bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  if (bad) return cleanup(fail(AQP_EINVAL, "index out of range in CSR upload"));
+  std::memset(&p->info, 0, sizeof(p->info));
+  p->info.a_nnz = d->a_nnz;
+  p->info.at_nnz = p->At.nnz;
+  p->info.q_full_nnz = p->q_full_nnz;
+  p->info.r_rows = d->r_rows;
+  p->info.quad_kind = d->quad_kind;
+  p->info.a_items = p->A.nitems;
+  p->info.at_items = p->At.nitems;
+  p->info.q_items = p->Q.nitems;
+  p->info.persistent_bytes = b.used;
+  *out = p;
+  return AQP_OK;
+}
+
+int aqp_problem_get_info(const aqp_problem *p, aqp_problem_info *out) {
+  if (!p || !out) return fail(AQP_EINVAL, "NULL argument");
+  *out = p->info;
+  return AQP_OK;
+}
+
+int aqp_problem_destroy(aqp_problem *p) {
+  delete p;
+  return AQP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1281 @@
+// aqp_solver.cu -- the device-resident PDHCG-II iteration (reference
+// anchorqp/engine.py:207-245,395-428, inner.py:84-134, certify.py:63-164).
+//
+// One certification window (<= check_every outer iterations) is ONE CUDA
+// graph launch:
+//
+//   WHILE(iterations left && !halted) {                       outer node
+//     P1  : A'y SpMV, epilogue lin = c + A'y and x0 = clamp(x)
+//           (diagonal Q: + closed-form prox, xbar, Halpern, |z-x|^2, window sum)
+//     G0  : Q x0 SpMV, epilogue g0 + 4 reductions -> res0, phi0, alpha0   (BB only)
+//     WHILE(bb continue) { S: x_t = clamp(x - alpha g);  G: Q x_t SpMV + gradient
+//                          epilogue + 7 reductions -> BB1/BB2 step, best-phi,
+//                          stop test on the device }                      (BB only)
+//     X   : xbar = 2x+ - x, Halpern, |z-x|^2, window sum, tolerance update (BB only)
+//     P2  : A xbar SpMV, epilogue dual step + Halpern(y) + window sum, slot rotation
+//   }
+//
+// All scalars (alpha, best phi, tolerances, counters, slot indices) live in a
+// device control block; the host only reads it at certification points.
+#include <cmath>
+#include <cstddef>
+#include <cstring>
+#include <vector>
+
+#include "aqp_common.cuh"
+#include "aqp_internal.h"
+#include "aqp_kernels.cuh"
+
+namespace aqp {
+
+// ---------------------------------------------------------------- control block
+enum RedSlot : int {
+  // residual ingredients
+  R_PV = 0, R_DV, R_QXI, R_ATYI, R_PRP, R_PRN, R_PRB, R_PYP, R_PYN, R_PYB, R_XQX, R_CX, R_PIDX, R_PIDY,
+  // y-ray j (base + 9j): norm, viol, aty_inf, var pos/neg/bad, con pos/neg/bad
+  R_YR = 16,
+  // x-ray j (base + 5j): norm, improvement, viol_x, viol_s, qd_inf
+  R_XR = 40,
+  // power iteration
+  R_PW = 56,
+  R_COUNT = 64
+};
+
+struct Ctrl {
+  aqp_scalars s;         // host-visible part (include/aqp.h)
+  double tau, sigma;     // eta/omega, eta*omega (engine.py:148-154), set by the host
+  int xcur, xprev, ycur, yprev;
+  int bb_cur, bb_best, bb_new, g_cur, g_new, bb_t, bb_xplus, pad0;
+  double alpha, alpha0, target, best_phi, best_res, phi, res, move;
+  int64_t window_len;
+  int pw_stop, pad1;
+  double red[R_COUNT];
+};
+
+struct SV {
+  // problem (read-only)
+  const double *c, *vlo, *vhi, *qd, *clo, *chi;
+  const int8_t *cone_r, *recc_x, *cone_y, *recc_s;
+  // iterate slots and companions
+  double *xs[3], *ys[3];
+  double *anc_x, *anc_y;   // anchor == round start (always equal in engine.py)
+  double *xlast, *ylast, *xblk, *yblk, *xavgp, *yavgp;
+  double *lin, *xbar, *xbb[3], *gbb[2];
+  double *rx, *rtv;        // low-rank temporaries (k and n)
+  double *xeval, *qx, *aty, *rs, *dx[2], *dy[2];
+  double *tm;              // m-length temporary (power iteration)
+  Ctrl *ctrl;
+  // constants
+  double eps_tol, gamma, tol_scale, tol_floor, diag_bound;
+  int adaptive, max_inner, halpern, quad_kind;
+  int64_t n, m;
+  cudaGraphConditionalHandle bb_cond, outer_cond;
+};
+
+
+// slot selection without dynamic indexing (keeps the op out of local memory)
+template <class T>
+__host__ __device__ __forceinline__ T pick3(T const (&a)[3], int i) { return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]); }
+template <class T>
+__host__ __device__ __forceinline__ T pick2(T const (&a)[2], int i) { return i == 0 ? a[0] : a[1]; }
+
+__device__ __forceinline__ void halpern_coefs(const Ctrl *ct, double &a, double &b, double &c3) {
+  // engine.py:239-244: a = (1+theta)*((k+1)/(k+2)), b = (1+theta)*(1/(k+2)), c = -theta
+  const double k = (double)ct->s.k, th = ct->s.theta;
+  a = (1.0 + th) * ((k + 1.0) / (k + 2.0));
+  b = (1.0 + th) * (1.0 / (k + 2.0));
+  c3 = -th;
+}
+
+// the x-side end of one outer iteration (engine.py:404-419): count, finiteness,
+// adaptive tolerance.  Runs in thread 0 of the last block of P1(diag) / X.
+__device__ __forceinline__ void x_iteration_end(const SV &v, double move2, int inner_iters) {
+  Ctrl *ct = v.ctrl;
+  const double move = sqrt(move2);
+  ct->move = move;
+  ct->s.iters_done += 1;
+  ct->s.inner_sum += inner_iters;
+  if (!isfinite(move)) {
+    ct->s.halted = 1;
+    return;
+  }
+  if (v.adaptive) {
+    // inner.py:41-48  min(current, max(scale*omega*move/tau, floor))
+    const double cand = py_max(v.tol_scale * ct->s.omega * move / ct->tau, v.tol_floor);
+    ct->s.inner_tol = py_min(ct->s.inner_tol, cand);
+  }
+}
+
+// z = Halpern/plain combination of one coordinate (engine.py:230-245, 400-403)
+struct Combine {
+  bool plain;
+  double a, b, c3;
+  bool use_prev;
+  __device__ __forceinline__ void init(const SV &v) {
+    const Ctrl *ct = v.ctrl;
+    plain = ct->s.probing || !v.halpern;
+    halpern_coefs(ct, a, b, c3);
+    use_prev = ct->s.theta != 0.0;
+  }
+  // lincomb3 of _core.pyx:160-170: (a*w + b*anchor) + c*prev
+  __device__ __forceinline__ double operator()(double w, const double *anc, const double *prev, int i) const {
+    if (plain) return w;
+    double z = a * w + b * anc[i];
+    if (use_prev) z = z + c3 * prev[i];
+    return z;
+  }
+};
+
+// ================================================================ iteration ops
+// P1 (BB path): lin = c + A'y ; x0 = clamp(x)
+struct OpP1Bb {
+  static constexpr int NS = 0, NM = 0;
+  static constexpr bool SYM = false, FINAL = false;
+  SV v;
+  const double *y;
+  const double *x;
+  __device__ bool skip() const { return v.ctrl->s.halted != 0; }
+  __device__ void prepare() {
+    y = pick3(v.ys, v.ctrl->ycur);
+    x = pick3(v.xs, v.ctrl->xcur);
+  }
+  __device__ double gather(int c) const { return __ldg(y + c); }
+  __device__ void row(int r, double s, RedVals<0, 0> &) const {
+    v.lin[r] = v.c[r] + s;  // engine.py:214 cost + A'y
+    pick3(v.xbb, 0)[r] = clip(x[r], v.vlo[r], v.vhi[r]);  // inner.py:94
+  }
+  __device__ void finalize(const RedVals<0, 0> &) const {}
+};
+
+// P1 (diagonal Q): the whole primal half of the step in one pass
+// (engine.py:213-222 with inner.py:69-81, 230-245, 404-428)
+struct OpP1Diag {
+  static constexpr int NS = 1, NM = 0;
+  static constexpr bool SYM = false, FINAL = true;
+  SV v;
+  const double *y, *x, *xprev;
+  double *znew;
+  double tau;
+  Combine cb;
+  __device__ bool skip() const { return v.ctrl->s.halted != 0; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    y = pick3(v.ys, ct->ycur);
+    x = pick3(v.xs, ct->xcur);
+    xprev = pick3(v.xs, ct->xprev);
+    znew = pick3(v.xs, 3 - ct->xcur - ct->xprev);
+    tau = ct->tau;
+    cb.init(v);
+  }
+  __device__ double gather(int c) const { return __ldg(y + c); }
+  __device__ void row(int r, double s, RedVals<1, 0> &acc) const {
+    const double lin = v.c[r] + s;
+    const double xk = x[r];
+    const double xp = clip((xk - tau * lin) / (1.0 + tau * v.qd[r]), v.vlo[r], v.vhi[r]);  // _core.pyx:127
+    v.xbar[r] = 2.0 * xp + (-1.0) * xk;                                                     // axpby
+    const double z = cb(xp, v.anc_x, xprev, r);
+    const double d = z - xk;
+    acc.s[0] += d * d;
+    v.xblk[r] += z;
+    znew[r] = z;
+  }
+  __device__ void finalize(const RedVals<1, 0> &t) const { x_iteration_end(v, t.s[0], 0); }
+};
+
+// Q-operator row value: P/Q row sum plus the low-rank correction (linalg.py:251-254)
+__device__ __forceinline__ double quad_row(const SV &v, int r, double s) {
+  return v.quad_kind == AQP_QUAD_SPARSE_LOW_RANK ? s + v.rtv[r] : s;
+}
+
+// G: Q x_t SpMV with the gradient epilogue and the BB reductions (inner.py:61-66,105-124)
+template <bool INIT>
+struct OpGrad {
+  static constexpr int NS = INIT ? 4 : 7, NM = 0;
+  static constexpr bool SYM = true, FINAL = true;
+  SV v;
+  const double *xt, *cen, *xo, *go;
+  double *gt;
+  double tau;
+  __device__ bool skip() const { return v.ctrl->s.halted != 0; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    xt = INIT ? pick3(v.xbb, 0) : pick3(v.xbb, ct->bb_new);
+    gt = INIT ? pick2(v.gbb, 0) : pick2(v.gbb, ct->g_new);
+    xo = pick3(v.xbb, ct->bb_cur);
+    go = pick2(v.gbb, ct->g_cur);
+    cen = pick3(v.xs, ct->xcur);
+    tau = ct->tau;
+  }
+  __device__ double gather(int c) const { return __ldg(xt + c); }
+  __device__ void row(int r, double s, RedVals<NS, 0> &acc) const {
+    const double qx = quad_row(v, r, s);
+    const double x = xt[r], c = cen[r], l = v.lin[r];
+    const double g = (qx + l) + (x - c) / tau;  // SubproblemSpec.gradient
+    gt[r] = g;
+    const double nr = x - clip(x - g, v.vlo[r], v.vhi[r]);  // natural_res_sq
+    acc.s[0] += nr * nr;
+    acc.s[1] += x * g;
+    acc.s[2] += l * x;
+    acc.s[3] += (x - c) * c;
+    if constexpr (!INIT) {
+      const double sd = x - xo[r], vd = g - go[r];
+      acc.s[4] += sd * vd;
+      acc.s[5] += sd * sd;
+      acc.s[6] += vd * vd;
+    }
+  }
+  __device__ void finalize(const RedVals<NS, 0> &t) const {
+    Ctrl *ct = v.ctrl;
+    const double res = sqrt(t.s[0]);
+    const double phi = 0.5 * ((t.s[1] + t.s[2]) - t.s[3] / tau);  // objective_from_gradient
+    ct->res = res;
+    ct->phi = phi;
+    unsigned cont = 0;
+    if (INIT) {
+      // solve_bb prologue, inner.py:92-104
+      ct->s.probing ? ct->target = py_min(ct->s.inner_tol, 1e-12) : ct->target = ct->s.inner_tol;
+      ct->best_phi = phi;
+      ct->best_res = res;
+      ct->bb_cur = 0;
+      ct->bb_best = 0;
+      ct->g_cur = 0;
+      ct->bb_t = 0;
+      ct->bb_xplus = 0;
+      if (res <= ct->target || v.max_inner <= 0) {
+        cont = 0;
+      } else {
+        ct->alpha0 = tau / (1.0 + tau * v.diag_bound);
+        ct->alpha = ct->alpha0;
+        ct->bb_new = 1;
+        ct->g_new = 1;
+        cont = 1;
+      }
+    } else {
+      // one BB iteration's bookkeeping, inner.py:110-124
+      const int t_ = ++ct->bb_t;
+      const int newslot = ct->bb_new;
+      if (phi < ct->best_phi) {
+        ct->best_phi = phi;
+        ct->bb_best = newslot;
+        ct->best_res = res;
+      }
+      const double sv = t.s[4];
+      double alpha;
+      if (sv > 0.0) {
+        alpha = (t_ % 2 == 1) ? t.s[5] / sv : sv / t.s[6];
+        alpha = py_min(py_max(alpha, 1e-10), 1e10);  // BB_STEP_MIN/MAX
+      } else {
+        alpha = ct->alpha0;
+      }
+      ct->alpha = alpha;
+      ct->bb_cur = newslot;
+      ct->g_cur = ct->g_new;
+      const bool conv = res <= ct->target;
+      if (conv || t_ >= v.max_inner) {
+        // return rule, inner.py:129-134
+        const double noise = 64.0 * 2.220446049250313e-16 * (1.0 + fabs(ct->best_phi));
+        if ((conv && phi <= ct->best_phi + noise) || phi <= ct->best_phi)
+          ct->bb_xplus = ct->bb_cur;
+        else
+          ct->bb_xplus = ct->bb_best;
+        cont = 0;
+      } else {
+        int nw = 0;
+        while (nw == ct->bb_cur || nw == ct->bb_best) ++nw;
+        ct->bb_new = nw;
+        ct->g_new = 1 - ct->g_cur;
+        cont = 1;
+      }
+    }
+    cudaGraphSetConditional(v.bb_cond, cont);
+  }
+};
+
+// S: x_t = clamp(x - alpha g)  (inner.py:106)
+struct OpStep {
+  static constexpr int NS = 0, NM = 0;
+  static constexpr bool FINAL = false;
+  SV v;
+  const double *xo, *go;
+  double *xn;
+  double alpha;
+  __device__ bool skip() const { return v.ctrl->s.halted != 0; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    xo = pick3(v.xbb, ct->bb_cur);
+    go = pick2(v.gbb, ct->g_cur);
+    xn = pick3(v.xbb, ct->bb_new);
+    alpha = ct->alpha;
+  }
+  __device__ void elem(int64_t i, RedVals<0, 0> &) const { xn[i] = clip(xo[i] - alpha * go[i], v.vlo[i], v.vhi[i]); }
+  __device__ void finalize(const RedVals<0, 0> &) const {}
+};
+
+// X: primal epilogue after the BB solve (engine.py:222, 230-245, 404-428)
+struct OpXPost {
+  static constexpr int NS = 1, NM = 0;
+  static constexpr bool FINAL = true;
+  SV v;
+  const double *xp, *x, *xprev;
+  double *znew;
+  Combine cb;
+  __device__ bool skip() const { return v.ctrl->s.halted != 0; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    xp = pick3(v.xbb, ct->bb_xplus);
+    x = pick3(v.xs, ct->xcur);
+    xprev = pick3(v.xs, ct->xprev);
+    znew = pick3(v.xs, 3 - ct->xcur - ct->xprev);
+    cb.init(v);
+  }
+  __device__ void elem(int64_t i, RedVals<1, 0> &acc) const {
+    const double p = xp[i], xk = x[i];
+    v.xbar[i] = 2.0 * p + (-1.0) * xk;
+    const double z = cb(p, v.anc_x, xprev, (int)i);
+    const double d = z - xk;
+    acc.s[0] += d * d;
+    v.xblk[i] += z;
+    znew[i] = z;
+  }
+  __device__ void finalize(const RedVals<1, 0> &t) const { x_iteration_end(v, t.s[0], v.ctrl->bb_t); }
+};
+
+// P2: y+ = dual_step(y, A xbar), Halpern(y), window sum; then slot rotation and
+// the outer-loop condition (engine.py:223-226, 420-428)
+struct OpP2 {
+  static constexpr int NS = 0, NM = 0;
+  static constexpr bool SYM = false, FINAL = true;
+  SV v;
+  const double *y, *yprev;
+  double *ynew;
+  double sigma;
+  Combine cb;
+  bool halted;
+  __device__ bool skip() const { return false; }  // must reach finalize to close the loop
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    halted = ct->s.halted != 0;
+    y = pick3(v.ys, ct->ycur);
+    yprev = pick3(v.ys, ct->yprev);
+    ynew = pick3(v.ys, 3 - ct->ycur - ct->yprev);
+    sigma = ct->sigma;
+    cb.init(v);
+  }
+  __device__ double gather(int c) const { return halted ? 0.0 : __ldg(v.xbar + c); }
+  __device__ void row(int r, double s, RedVals<0, 0> &) const {
+    if (halted) return;
+    const double w = y[r] / sigma + s;                                  // _core.pyx:155
+    const double yp = sigma * (w - clip(w, v.clo[r], v.chi[r]));        // _core.pyx:156
+    const double z = cb(yp, v.anc_y, yprev, r);
+    v.yblk[r] += z;
+    ynew[r] = z;
+  }
+  __device__ void finalize(const RedVals<0, 0> &) const {
+    Ctrl *ct = v.ctrl;
+    if (ct->s.halted) {
+      cudaGraphSetConditional(v.outer_cond, 0u);
+      return;
+    }
+    const int xn = 3 - ct->xcur - ct->xprev, yn = 3 - ct->ycur - ct->yprev;
+    ct->xprev = ct->xcur;
+    ct->xcur = xn;
+    ct->yprev = ct->ycur;
+    ct->ycur = yn;
+    if (!ct->s.probing) ct->s.k += 1;
+    ct->s.block_len += 1;
+    cudaGraphSetConditional(v.outer_cond, ct->s.iters_done < ct->window_len ? 1u : 0u);
+  }
+};
+
+// low-rank: rx = R x (k outputs) and rtv = R' rx (n outputs), linalg.py:251-254
+struct OpRx {
+  static constexpr int NS = 0, NM = 0;
+  static constexpr bool SYM = false, FINAL = false;
+  SV v;
+  int src;  // 0: BB x0, 1: BB x_new, 2: x_eval, 3/4: x-ray candidate 0/1
+  const double *x;
+  __device__ bool skip() const { return src < 2 && v.ctrl->s.halted != 0; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    x = src == 0 ? pick3(v.xbb, 0) : src == 1 ? pick3(v.xbb, ct->bb_new) : src == 2 ? v.xeval : pick2(v.dx, src - 3);
+  }
+  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ void row(int r, double s, RedVals<0, 0> &) const { v.rx[r] = s; }
+  __device__ void finalize(const RedVals<0, 0> &) const {}
+};
+
+struct OpRtv {
+  static constexpr int NS = 0, NM = 0;
+  static constexpr bool SYM = false, FINAL = false;
+  SV v;
+  int src;
+  __device__ bool skip() const { return src < 2 && v.ctrl->s.halted != 0; }
+  __device__ void prepare() {}
+  __device__ double gather(int c) const { return __ldg(v.rx + c); }
+  __device__ void row(int r, double s, RedVals<0, 0> &) const { v.rtv[r] = s; }
+  __device__ void finalize(const RedVals<0, 0> &) const {}
+};
+
+// ================================================================ certification ops
+__device__ __forceinline__ bool cand_valid(const Ctrl *ct, int j, double norm) {
+  return (j == 1 || ct->s.have_avg_prev) && norm != 0.0 && isfinite(norm);
+}
+
+// x side: x_eval, window average, candidate differences, PID norm (engine.py:436-453, 267)
+struct OpChkX {
+  static constexpr int NS = 1, NM = 2;
+  static constexpr bool FINAL = true;
+  SV v;
+  int rays;
+  const double *x;
+  double inv_len;
+  double len;
+  int have_prev;
+  __device__ bool skip() const { return false; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    x = pick3(v.xs, ct->xcur);
+    len = (double)ct->s.block_len;
+    have_prev = ct->s.have_avg_prev;
+  }
+  __device__ void elem(int64_t i, RedVals<1, 2> &acc) const {
+    const double xi = x[i];
+    v.xeval[i] = clip(xi, v.vlo[i], v.vhi[i]);
+    const double dr = xi - v.anc_x[i];
+    acc.s[0] += dr * dr;
+    if (rays) {
+      const double avg = v.xblk[i] / len;
+      if (have_prev) {
+        const double d0 = avg - v.xavgp[i];
+        pick2(v.dx, 0)[i] = d0;
+        acc.m[0] = nanmax(acc.m[0], fabs(d0));
+      }
+      v.xavgp[i] = avg;
+      v.xblk[i] = 0.0;
+      const double d1 = xi - v.xlast[i];
+      pick2(v.dx, 1)[i] = d1;
+      acc.m[1] = nanmax(acc.m[1], fabs(d1));
+    }
+  }
+  __device__ void finalize(const RedVals<1, 2> &t) const {
+    double *red = v.ctrl->red;
+    red[R_PIDX] = t.s[0];
+    red[R_XR + 0] = t.m[0];
+    red[R_XR + 5] = t.m[1];
+  }
+};
+
+// y side: PID norm, p(proj_Y y), window average, projected candidates
+struct OpChkY {
+  static constexpr int NS = 4, NM = 2;
+  static constexpr bool FINAL = true;
+  SV v;
+  int rays;
+  const double *y;
+  double len;
+  int have_prev;
+  __device__ bool skip() const { return false; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    y = pick3(v.ys, ct->ycur);
+    len = (double)ct->s.block_len;
+    have_prev = ct->s.have_avg_prev;
+  }
+  __device__ void elem(int64_t i, RedVals<4, 2> &acc) const {
+    const double yi = y[i];
+    const int8_t cy = v.cone_y[i];
+    const double dr = yi - v.anc_y[i];
+    acc.s[0] += dr * dr;
+    double bad = acc.s[3];
+    support_add(cone_proj(yi, cy), v.clo[i], v.chi[i], acc.s[1], acc.s[2], bad);
+    acc.s[3] = bad;
+    if (rays) {
+      const double avg = v.yblk[i] / len;
+      if (have_prev) {
+        const double p0 = cone_proj(avg - v.yavgp[i], cy);
+        pick2(v.dy, 0)[i] = p0;
+        acc.m[0] = nanmax(acc.m[0], fabs(p0));
+      }
+      v.yavgp[i] = avg;
+      v.yblk[i] = 0.0;
+      const double p1 = cone_proj(yi - v.ylast[i], cy);
+      pick2(v.dy, 1)[i] = p1;
+      acc.m[1] = nanmax(acc.m[1], fabs(p1));
+    }
+  }
+  __device__ void finalize(const RedVals<4, 2> &t) const {
+    double *red = v.ctrl->red;
+    red[R_PIDY] = t.s[0];
+    red[R_PYP] = t.s[1];
+    red[R_PYN] = t.s[2];
+    red[R_PYB] = t.s[3] > 0.0 ? 1.0 : 0.0;
+    red[R_YR + 0] = t.m[0];
+    red[R_YR + 9] = t.m[1];
+  }
+};
+
+// A x_eval: primal violation; with rays also normalise the y candidates and
+// take p(ray; l_c, u_c) (certify.py:66,75-77,120,131)
+struct OpChkA {
+  static constexpr int NS = 6, NM = 1;
+  static constexpr bool SYM = false, FINAL = true;
+  SV v;
+  int rays;
+  double nrm[2];
+  bool ok[2];
+  __device__ bool skip() const { return false; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    for (int j = 0; j < 2; ++j) {
+      nrm[j] = ct->red[R_YR + 9 * j];
+      ok[j] = rays && cand_valid(ct, j, nrm[j]);
+    }
+  }
+  __device__ double gather(int c) const { return __ldg(v.xeval + c); }
+  __device__ void row(int r, double s, RedVals<6, 1> &acc) const {
+    acc.m[0] = nanmax(acc.m[0], fabs(s - clip(s, v.clo[r], v.chi[r])));
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (!ok[j]) continue;
+      const double ray = pick2(v.dy, j)[r] / nrm[j];
+      pick2(v.dy, j)[r] = ray;
+      double bad = acc.s[3 * j + 2];
+      support_add(ray, v.clo[r], v.chi[r], acc.s[3 * j], acc.s[3 * j + 1], bad);
+      acc.s[3 * j + 2] = bad;
+    }
+  }
+  __device__ void finalize(const RedVals<6, 1> &t) const {
+    double *red = v.ctrl->red;
+    red[R_PV] = t.m[0];
+    for (int j = 0; j < 2; ++j) {
+      red[R_YR + 9 * j + 6] = t.s[3 * j];
+      red[R_YR + 9 * j + 7] = t.s[3 * j + 1];
+      red[R_YR + 9 * j + 8] = t.s[3 * j + 2] > 0.0 ? 1.0 : 0.0;
+    }
+  }
+};
+
+// plain stores of an SpMV result: Q x_eval -> qx, A'y -> aty, A v -> tm, ...
+struct OpStore {
+  static constexpr int NS = 1, NM = 0;
+  static constexpr bool SYM_ = false;
+  static constexpr bool FINAL = true;
+  SV v;
+  int src;   // gather source: 0 x_eval, 1 y (current), 2 power-iteration v (xbb[1]), 3 tm
+  int dst;   // 0 qx (adds low-rank part), 1 aty, 2 tm, 3 xbb[2]
+  int red;   // reduction slot for sum of squares of the output (or -1)
+  const double *x;
+  double *out;
+  __device__ bool skip() const { return src >= 2 && v.ctrl->pw_stop; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    x = src == 0 ? v.xeval : src == 1 ? pick3(v.ys, ct->ycur) : src == 2 ? pick3(v.xbb, 1) : v.tm;
+    out = dst == 0 ? v.qx : dst == 1 ? v.aty : dst == 2 ? v.tm : pick3(v.xbb, 2);
+  }
+  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ void row(int r, double s, RedVals<1, 0> &acc) const {
+    const double o = dst == 0 ? quad_row(v, r, s) : s;
+    out[r] = o;
+    acc.s[0] += o * o;
+  }
+  __device__ void finalize(const RedVals<1, 0> &t) const {
+    if (red >= 0) v.ctrl->red[red] = t.s[0];
+  }
+};
+template <bool S>
+struct OpStoreT : OpStore {
+  static constexpr bool SYM = S;
+};
+
+// dual residual, gap ingredients, dual slack; x-ray normalisation (certify.py:67-95,148-157)
+struct OpChkR {
+  static constexpr int NS = 7, NM = 5;
+  static constexpr bool FINAL = true;
+  SV v;
+  int rays;
+  double nrm[2];
+  bool ok[2];
+  __device__ bool skip() const { return false; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    for (int j = 0; j < 2; ++j) {
+      nrm[j] = ct->red[R_XR + 5 * j];
+      ok[j] = rays && cand_valid(ct, j, nrm[j]);
+    }
+  }
+  __device__ void elem(int64_t i, RedVals<7, 5> &acc) const {
+    const double x = v.xeval[i];
+    double q;
+    if (v.quad_kind == AQP_QUAD_DIAGONAL) {
+      q = v.qd[i] * x;
+      v.qx[i] = q;
+    } else {
+      q = v.qx[i];
+    }
+    const double at = v.aty[i], c = v.c[i];
+    const double r = (q + c) + at;
+    v.rs[i] = r;
+    const double rp = cone_proj(r, v.cone_r[i]);
+    acc.m[0] = nanmax(acc.m[0], fabs(r - rp));
+    acc.m[1] = nanmax(acc.m[1], fabs(q));
+    acc.m[2] = nanmax(acc.m[2], fabs(at));
+    double bad = acc.s[2];
+    support_add(-rp, v.vlo[i], v.vhi[i], acc.s[0], acc.s[1], bad);
+    acc.s[2] = bad;
+    acc.s[3] += x * q;
+    acc.s[4] += c * x;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (!ok[j]) continue;
+      const double d = pick2(v.dx, j)[i] / nrm[j];
+      pick2(v.dx, j)[i] = d;
+      acc.s[5 + j] += c * d;
+      acc.m[3 + j] = nanmax(acc.m[3 + j], fabs(d - cone_proj(d, v.recc_x[i])));
+    }
+  }
+  __device__ void finalize(const RedVals<7, 5> &t) const {
+    double *red = v.ctrl->red;
+    red[R_PRP] = t.s[0];
+    red[R_PRN] = t.s[1];
+    red[R_PRB] = t.s[2] > 0.0 ? 1.0 : 0.0;
+    red[R_XQX] = t.s[3];
+    red[R_CX] = t.s[4];
+    red[R_DV] = t.m[0];
+    red[R_QXI] = t.m[1];
+    red[R_ATYI] = t.m[2];
+    for (int j = 0; j < 2; ++j) {
+      red[R_XR + 5 * j + 1] = t.s[5 + j];
+      red[R_XR + 5 * j + 2] = t.m[3 + j];
+    }
+  }
+};
+
+// y-ray test body: A' ray (certify.py:121-127)
+struct OpChkYRay {
+  static constexpr int NS = 3, NM = 2;
+  static constexpr bool SYM = false, FINAL = true;
+  SV v;
+  int j;
+  const double *ray;
+  __device__ bool skip() const {
+    const Ctrl *ct = v.ctrl;
+    return !cand_valid(ct, j, ct->red[R_YR + 9 * j]);
+  }
+  __device__ void prepare() { ray = pick2(v.dy, j); }
+  __device__ double gather(int c) const { return __ldg(ray + c); }
+  __device__ void row(int r, double s, RedVals<3, 2> &acc) const {
+    const double p = cone_proj(s, v.cone_r[r]);
+    acc.m[0] = nanmax(acc.m[0], fabs(s - p));
+    acc.m[1] = nanmax(acc.m[1], fabs(s));
+    double bad = acc.s[2];
+    support_add(-p, v.vlo[r], v.vhi[r], acc.s[0], acc.s[1], bad);
+    acc.s[2] = bad;
+  }
+  __device__ void finalize(const RedVals<3, 2> &t) const {
+    double *red = v.ctrl->red + R_YR + 9 * j;
+    red[1] = t.m[0];
+    red[2] = t.m[1];
+    red[3] = t.s[0];
+    red[4] = t.s[1];
+    red[5] = t.s[2] > 0.0 ? 1.0 : 0.0;
+  }
+};
+
+// x-ray test body: A d and Q d (certify.py:158-160); skipped unless c'd < -eps_tol
+struct OpChkXRay {
+  static constexpr int NS = 0, NM = 1;
+  static constexpr bool FINAL = true;
+  SV v;
+  int j;
+  int which;  // 0: A d (recession of S), 1: Q d
+  const double *d;
+  __device__ bool skip() const {
+    const Ctrl *ct = v.ctrl;
+    const double *xr = ct->red + R_XR + 5 * j;
+    return !(cand_valid(ct, j, xr[0]) && xr[1] < -v.eps_tol);
+  }
+  __device__ void prepare() { d = pick2(v.dx, j); }
+  __device__ double gather(int c) const { return __ldg(d + c); }
+  __device__ void row(int r, double s, RedVals<0, 1> &acc) const {
+    if (which == 0) {
+      acc.m[0] = nanmax(acc.m[0], fabs(s - cone_proj(s, v.recc_s[r])));
+    } else {
+      acc.m[0] = nanmax(acc.m[0], fabs(quad_row(v, r, s)));
+    }
+  }
+  __device__ void elem(int64_t i, RedVals<0, 1> &acc) const {  // diagonal Q: |q_i d_i|
+    acc.m[0] = nanmax(acc.m[0], fabs(v.qd[i] * d[i]));
+  }
+  __device__ void finalize(const RedVals<0, 1> &t) const {
+    v.ctrl->red[R_XR + 5 * j + 3 + which] = t.m[0];
+  }
+};
+template <bool S>
+struct OpChkXRayT : OpChkXRay {
+  static constexpr bool SYM = S;
+};
+
+struct OpXRayRx : OpRx {
+  int j;
+  __device__ bool skip() const {
+    const Ctrl *ct = v.ctrl;
+    const double *xr = ct->red + R_XR + 5 * j;
+    return !(cand_valid(ct, j, xr[0]) && xr[1] < -v.eps_tol);
+  }
+};
+struct OpXRayRtv : OpRtv {
+  int j;
+  __device__ bool skip() const {
+    const Ctrl *ct = v.ctrl;
+    const double *xr = ct->red + R_XR + 5 * j;
+    return !(cand_valid(ct, j, xr[0]) && xr[1] < -v.eps_tol);
+  }
+};
+
+// ---------------------------------------------------------------- state transitions
+struct OpState {
+  static constexpr int NS = 0, NM = 0;
+  static constexpr bool FINAL = false;
+  SV v;
+  int side;  // 0: n side, 1: m side
+  int mode;  // 0 init, 1 mark cert, 2 restart/reanchor, 3 rollback
+  double *cur, *prev, *anc, *last, *blk, *avgp, *spare;
+  __device__ bool skip() const { return false; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    if (side == 0) {
+      cur = pick3(v.xs, ct->xcur); prev = pick3(v.xs, ct->xprev); spare = pick3(v.xs, 3 - ct->xcur - ct->xprev);
+      anc = v.anc_x; last = v.xlast; blk = v.xblk; avgp = v.xavgp;
+    } else {
+      cur = pick3(v.ys, ct->ycur); prev = pick3(v.ys, ct->yprev); spare = pick3(v.ys, 3 - ct->ycur - ct->yprev);
+      anc = v.anc_y; last = v.ylast; blk = v.yblk; avgp = v.yavgp;
+    }
+  }
+  __device__ void elem(int64_t i, RedVals<0, 0> &) const {
+    switch (mode) {
+      case 0: {  // engine.py:174-204: x0 = clamp(0), y0 = 0
+        const double z = side == 0 ? clip(0.0, v.vlo[i], v.vhi[i]) : 0.0;
+        cur[i] = z; prev[i] = z; spare[i] = z; anc[i] = z; last[i] = z; blk[i] = 0.0; avgp[i] = 0.0;
+        break;
+      }
+      case 1: last[i] = cur[i]; break;
+      case 2: { const double z = cur[i]; anc[i] = z; prev[i] = z; break; }
+      case 3: { const double z = anc[i]; cur[i] = z; prev[i] = z; break; }
+      default: blk[i] = 0.0; break;
+    }
+  }
+  __device__ void finalize(const RedVals<0, 0> &) const {}
+};
+
+// ---------------------------------------------------------------- power iteration ops
+struct OpPwNorm {  // sum of squares of xbb[idx] -> red[slot]
+  static constexpr int NS = 1, NM = 0;
+  static constexpr bool FINAL = true;
+  SV v;
+  int idx, slot;
+  const double *x;
+  __device__ bool skip() const { return v.ctrl->pw_stop != 0; }
+  __device__ void prepare() { x = pick3(v.xbb, idx); }
+  __device__ void elem(int64_t i, RedVals<1, 0> &acc) const { acc.s[0] += x[i] * x[i]; }
+  __device__ void finalize(const RedVals<1, 0> &t) const { v.ctrl->red[slot] = t.s[0]; }
+};
+
+struct OpPwScale {  // xbb[dst] = xbb[src] / sqrt(red[slot]); stop when the norm is 0
+  static constexpr int NS = 0, NM = 0;
+  static constexpr bool FINAL = false;
+  SV v;
+  int src, dst, slot;
+  double nrm;
+  const double *x;
+  double *o;
+  __device__ bool skip() const { return v.ctrl->pw_stop != 0 || v.ctrl->red[slot] == 0.0; }
+  __device__ void prepare() {
+    nrm = sqrt(v.ctrl->red[slot]);
+    x = pick3(v.xbb, src);
+    o = pick3(v.xbb, dst);
+  }
+  __device__ void elem(int64_t i, RedVals<0, 0> &) const { o[i] = x[i] / nrm; }
+  __device__ void finalize(const RedVals<0, 0> &) const {}
+};
+
+__global__ void k_pw_check(Ctrl *ct, int slot) {
+  if (ct->red[slot] == 0.0) ct->pw_stop = 1;  // linalg.py:309 `if nw == 0.0: break`
+}
+
+}  // namespace aqp
+
+using namespace aqp;
+
+// ====================================================================== solver object
+struct aqp_solver {
+  aqp_problem *p = nullptr;
+  aqp_solver_params prm{};
+  SV v{};
+  Ctrl *d_ctrl = nullptr;
+  Ctrl h{};  // host mirror (valid after sync points)
+  GridRed gr{};
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches_per_iter_fixed = 0;
+  int64_t kernel_launches = 0;
+};
+
+namespace {
+
+void layout_solver(Bump &b, aqp_problem *p, SV &v, Ctrl **ctrl, GridRed &gr) {
+  const int64_t n = std::max<int64_t>(p->n, 1), m = std::max<int64_t>(p->m, 1);
+  auto vn = [&]() { return (double *)b.take(n * 8); };
+  auto vm = [&]() { return (double *)b.take(m * 8); };
+  for (int i = 0; i < 3; ++i) v.xs[i] = vn();
+  for (int i = 0; i < 3; ++i) v.ys[i] = vm();
+  v.anc_x = vn(); v.anc_y = vm();
+  v.xlast = vn(); v.ylast = vm();
+  v.xblk = vn(); v.yblk = vm();
+  v.xavgp = vn(); v.yavgp = vm();
+  v.lin = vn(); v.xbar = vn();
+  for (int i = 0; i < 3; ++i) v.xbb[i] = vn();
+  for (int i = 0; i < 2; ++i) v.gbb[i] = vn();
+  v.rx = (double *)b.take(std::max<int64_t>(p->R.rows, 1) * 8);
+  v.rtv = vn();
+  v.xeval = vn(); v.qx = vn(); v.aty = vn(); v.rs = vn();
+  v.dx[0] = vn(); v.dx[1] = vn();
+  v.dy[0] = vm(); v.dy[1] = vm();
+  v.tm = vm();
+  *ctrl = (Ctrl *)b.take(sizeof(Ctrl));
+  int64_t maxg = 148 * 8;
+  for (const DevCsr *M : {&p->A, &p->At, &p->Q, &p->R, &p->Rt}) maxg = std::max<int64_t>(maxg, M->nitems);
+  gr.partials = (double *)b.take(maxg * kMaxRed * 8);
+  gr.ticket = (unsigned *)b.take(64);
+}
+
+// explicit graph construction helpers
+template <class K, class... A>
+cudaError_t add_node(cudaGraph_t g, cudaGraphNode_t &last, unsigned grid, K fn, A... args) {
+  void *params[] = {(void *)&args...};
+  cudaKernelNodeParams kp = {};
+  kp.func = (void *)fn;
+  kp.gridDim = dim3(grid);
+  kp.blockDim = dim3(kThreads);
+  kp.sharedMemBytes = 0;
+  kp.kernelParams = params;
+  kp.extra = nullptr;
+  cudaGraphNode_t node;
+  cudaError_t e = cudaGraphAddKernelNode(&node, g, last ? &last : nullptr, last ? 1 : 0, &kp);
+  if (e == cudaSuccess) last = node;
+  return e;
+}
+
+template <class Op>
+cudaError_t node_spmv(cudaGraph_t g, cudaGraphNode_t &last, const DevCsr &M, const Op &op, GridRed gr) {
+  return add_node(g, last, (unsigned)M.nitems, spmv_op<Op>, M, op, gr);
+}
+template <class Op>
+cudaError_t node_elem(cudaGraph_t g, cudaGraphNode_t &last, int64_t n, const Op &op, GridRed gr) {
+  return add_node(g, last, (unsigned)elem_grid(n), elem_op<Op>, n, op, gr);
+}
+
+template <class Op>
+cudaError_t run_spmv(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
+  spmv_op<Op><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
+  return cudaGetLastError();
+}
+template <class Op>
+cudaError_t run_elem(cudaStream_t st, int64_t n, const Op &op, GridRed gr) {
+  elem_op<Op><<<elem_grid(n), kThreads, 0, st>>>(n, op, gr);
+  return cudaGetLastError();
+}
+
+int add_lowrank(aqp_solver *s, cudaGraph_t g, cudaGraphNode_t &last, int src) {
+  aqp_problem *p = s->p;
+  OpRx rx{};
+  rx.v = s->v;
+  rx.src = src;
+  OpRtv rt{};
+  rt.v = s->v;
+  rt.src = src;
+  AQP_CUDA(node_spmv(g, last, p->R, rx, s->gr));
+  AQP_CUDA(node_spmv(g, last, p->Rt, rt, s->gr));
+  return AQP_OK;
+}
+
+// Build the window graph: WHILE(outer) { one outer iteration }
+int build_graph(aqp_solver *s) {
+  aqp_problem *p = s->p;
+  cudaGraph_t g;
+  AQP_CUDA(cudaGraphCreate(&g, 0));
+  s->graph = g;
+  cudaGraphConditionalHandle hout, hbb;
+  AQP_CUDA(cudaGraphConditionalHandleCreate(&hout, g, 1u, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hout;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t outer;
+  AQP_CUDA(cudaGraphAddNode(&outer, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  s->v.outer_cond = hout;
+  const bool diag = p->quad_kind == AQP_QUAD_DIAGONAL;
+  const bool lowrank = p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK;
+  if (!diag) {
+    AQP_CUDA(cudaGraphConditionalHandleCreate(&hbb, body, 0u, cudaGraphCondAssignDefault));
+    s->v.bb_cond = hbb;
+  }
+  SV v = s->v;
+  GridRed gr = s->gr;
+  cudaGraphNode_t last = nullptr;
+  int64_t fixed = 0;
+  if (diag) {
+    OpP1Diag o{};
+    o.v = v;
+    AQP_CUDA(node_spmv(body, last, p->At, o, gr));
+    fixed += 1;
+  } else {
+    OpP1Bb o{};
+    o.v = v;
+    AQP_CUDA(node_spmv(body, last, p->At, o, gr));
+    if (lowrank) AQP_TRY(add_lowrank(s, body, last, 0));
+    OpGrad<true> g0{};
+    g0.v = v;
+    AQP_CUDA(node_spmv(body, last, p->Q, g0, gr));
+    fixed += 2 + (lowrank ? 2 : 0);
+    // inner WHILE
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hbb;
+    ip.conditional.type = cudaGraphCondTypeWhile;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inner;
+    AQP_CUDA(cudaGraphAddNode(&inner, body, &last, 1, &ip));
+    last = inner;
+    cudaGraph_t ib = ip.conditional.phGraph_out[0];
+    cudaGraphNode_t il = nullptr;
+    OpStep st{};
+    st.v = v;
+    AQP_CUDA(node_elem(ib, il, p->n, st, gr));
+    if (lowrank) AQP_TRY(add_lowrank(s, ib, il, 1));
+    OpGrad<false> gg{};
+    gg.v = v;
+    AQP_CUDA(node_spmv(ib, il, p->Q, gg, gr));
+    OpXPost xp{};
+    xp.v = v;
+    AQP_CUDA(node_elem(body, last, p->n, xp, gr));
+    fixed += 1;
+  }
+  OpP2 p2{};
+  p2.v = v;
+  AQP_CUDA(node_spmv(body, last, p->A, p2, gr));
+  fixed += 1;
+  s->launches_per_iter_fixed = fixed;
+  AQP_CUDA(cudaGraphInstantiate(&s->exec, g, 0));
+  return AQP_OK;
+}
+
+// Push only the host-owned prefix of the control block (aqp_scalars + tau,
+// sigma); device-owned fields (slots, BB state, reductions) are never
+// overwritten from a possibly stale host mirror.
+int push_scalars(aqp_solver *s) {
+  s->h.tau = s->h.s.eta / s->h.s.omega;    // engine.py:148-150
+  s->h.sigma = s->h.s.eta * s->h.s.omega;  // engine.py:152-154
+  AQP_CUDA(cudaMemcpyAsync(s->d_ctrl, &s->h, offsetof(Ctrl, xcur), cudaMemcpyHostToDevice, s->p->ctx->stream));
+  return AQP_OK;
+}
+
+template <class T>
+int poke(aqp_solver *s, T Ctrl::*field, T value) {
+  s->h.*field = value;
+  AQP_CUDA(cudaMemcpyAsync(&(s->d_ctrl->*field), &(s->h.*field), sizeof(T), cudaMemcpyHostToDevice,
+                           s->p->ctx->stream));
+  return AQP_OK;
+}
+
+// full push (only at init, when the host mirror is authoritative)
+int push_all(aqp_solver *s) {
+  s->h.tau = s->h.s.eta / s->h.s.omega;
+  s->h.sigma = s->h.s.eta * s->h.s.omega;
+  AQP_CUDA(cudaMemcpyAsync(s->d_ctrl, &s->h, sizeof(Ctrl), cudaMemcpyHostToDevice, s->p->ctx->stream));
+  AQP_CUDA(cudaStreamSynchronize(s->p->ctx->stream));
+  return AQP_OK;
+}
+
+int pull_ctrl(aqp_solver *s) {
+  cudaStream_t st = s->p->ctx->stream;
+  AQP_CUDA(cudaMemcpyAsync(&s->h, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  return AQP_OK;
+}
+
+int state_op(aqp_solver *s, int mode) {
+  cudaStream_t st = s->p->ctx->stream;
+  for (int side = 0; side < 2; ++side) {
+    OpState o{};
+    o.v = s->v;
+    o.side = side;
+    o.mode = mode;
+    AQP_CUDA(run_elem(st, side == 0 ? s->p->n : s->p->m, o, s->gr));
+  }
+  return AQP_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int aqp_solver_sizes(const aqp_problem *p, size_t *workspace_bytes) {
+  if (!p || !workspace_bytes) return fail(AQP_EINVAL, "NULL argument");
+  Bump b;
+  SV v{};
+  Ctrl *c = nullptr;
+  GridRed gr{};
+  layout_solver(b, const_cast<aqp_problem *>(p), v, &c, gr);
+  *workspace_bytes = b.used + 256;
+  return AQP_OK;
+}
+
+int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, size_t ws_bytes, aqp_solver **out) {
+  if (!p || !prm || !ws || !out) return fail(AQP_EINVAL, "NULL argument");
+  aqp_solver *s = new aqp_solver();
+  s->p = p;
+  s->prm = *prm;
+  Bump b;
+  b.base = ws;
+  b.cap = ws_bytes;
+  layout_solver(b, p, s->v, &s->d_ctrl, s->gr);
+  if (b.overflow) {
+    delete s;
+    return fail(AQP_ENOMEM, "solver workspace too small");
+  }
+  SV &v = s->v;
+  v.c = p->c; v.vlo = p->vlo; v.vhi = p->vhi; v.qd = p->qd; v.clo = p->clo; v.chi = p->chi;
+  v.cone_r = p->cone_r; v.recc_x = p->recc_x; v.cone_y = p->cone_y; v.recc_s = p->recc_s;
+  v.ctrl = s->d_ctrl;
+  v.eps_tol = prm->eps_tol;
+  v.gamma = prm->gamma_sys;
+  v.tol_scale = prm->tol_scale;
+  v.tol_floor = prm->tol_floor;
+  v.diag_bound = prm->diag_bound;
+  v.adaptive = prm->adaptive;
+  v.max_inner = prm->max_inner;
+  v.halpern = prm->halpern;
+  v.quad_kind = p->quad_kind;
+  v.n = p->n;
+  v.m = p->m;
+  std::memset(&s->h, 0, sizeof(Ctrl));
+  s->h.xcur = 0; s->h.xprev = 1; s->h.ycur = 0; s->h.yprev = 1;
+  cudaStream_t st = p->ctx->stream;
+  AQP_CUDA(cudaMemsetAsync(s->gr.ticket, 0, 64, st));
+  int rc = build_graph(s);
+  if (rc) {
+    delete s;
+    return rc;
+  }
+  *out = s;
+  return AQP_OK;
+}
+
+int aqp_solver_destroy(aqp_solver *s) {
+  if (!s) return AQP_OK;
+  if (s->exec) cudaGraphExecDestroy(s->exec);
+  if (s->graph) cudaGraphDestroy(s->graph);
+  delete s;
+  return AQP_OK;
+}
+
+int aqp_solver_init(aqp_solver *s, const aqp_scalars *sc) {
+  if (!s || !sc) return fail(AQP_EINVAL, "NULL argument");
+  s->h.s = *sc;
+  s->h.xcur = 0; s->h.xprev = 1; s->h.ycur = 0; s->h.yprev = 1;
+  s->h.pw_stop = 0;
+  AQP_TRY(push_all(s));
+  AQP_TRY(state_op(s, 0));
+  return AQP_OK;
+}
+
+int aqp_solver_set_scalars(aqp_solver *s, const aqp_scalars *sc) {
+  if (!s || !sc) return fail(AQP_EINVAL, "NULL argument");
+  s->h.s = *sc;
+  return push_scalars(s);
+}
+
+int aqp_solver_get_scalars(aqp_solver *s, aqp_scalars *sc) {
+  if (!s || !sc) return fail(AQP_EINVAL, "NULL argument");
+  AQP_TRY(pull_ctrl(s));
+  *sc = s->h.s;
+  return AQP_OK;
+}
+
+int aqp_solver_run(aqp_solver *s, int64_t n_iters) {
+  if (!s) return fail(AQP_EINVAL, "NULL argument");
+  if (n_iters <= 0) return AQP_OK;
+  // host mirror is current (the host only changes scalars between windows)
+  s->h.s.iters_done = 0;
+  s->h.s.inner_sum = 0;
+  AQP_TRY(push_scalars(s));
+  AQP_TRY(poke(s, &Ctrl::window_len, (int64_t)n_iters));
+  AQP_CUDA(cudaGraphLaunch(s->exec, s->p->ctx->stream));
+  return AQP_OK;
+}
+
+int aqp_solver_check(aqp_solver *s, int with_rays, aqp_check_result *out) {
+  if (!s || !out) return fail(AQP_EINVAL, "NULL argument");
+  aqp_problem *p = s->p;
+  cudaStream_t st = p->ctx->stream;
+  const SV &v = s->v;
+  GridRed gr = s->gr;
+  const int rays = with_rays ? 1 : 0;
+  AQP_CUDA(cudaMemsetAsync(&s->d_ctrl->red[0], 0, sizeof(double) * R_PW, st));
+  { OpChkX o{}; o.v = v; o.rays = rays; AQP_CUDA(run_elem(st, p->n, o, gr)); }
+  { OpChkY o{}; o.v = v; o.rays = rays; AQP_CUDA(run_elem(st, p->m, o, gr)); }
+  { OpChkA o{}; o.v = v; o.rays = rays; AQP_CUDA(run_spmv(st, p->A, o, gr)); }
+  if (p->quad_kind != AQP_QUAD_DIAGONAL) {
+    if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
+      OpRx rx{}; rx.v = v; rx.src = 2;
+      OpRtv rt{}; rt.v = v; rt.src = 2;
+      AQP_CUDA(run_spmv(st, p->R, rx, gr));
+      AQP_CUDA(run_spmv(st, p->Rt, rt, gr));
+    }
+    OpStoreT<true> q{}; q.v = v; q.src = 0; q.dst = 0; q.red = -1;
+    AQP_CUDA(run_spmv(st, p->Q, q, gr));
+  }
+  { OpStoreT<false> a{}; a.v = v; a.src = 1; a.dst = 1; a.red = -1; AQP_CUDA(run_spmv(st, p->At, a, gr)); }
+  { OpChkR o{}; o.v = v; o.rays = rays; AQP_CUDA(run_elem(st, p->n, o, gr)); }
+  if (rays) {
+    for (int j = 0; j < 2; ++j) {
+      OpChkYRay o{}; o.v = v; o.j = j;
+      AQP_CUDA(run_spmv(st, p->At, o, gr));
+    }
+    for (int j = 0; j < 2; ++j) {
+      OpChkXRayT<false> a{}; a.v = v; a.j = j; a.which = 0;
+      AQP_CUDA(run_spmv(st, p->A, a, gr));
+      if (p->quad_kind == AQP_QUAD_DIAGONAL) {
+        OpChkXRayT<false> q{}; q.v = v; q.j = j; q.which = 1;
+        AQP_CUDA(run_elem(st, p->n, q, gr));
+      } else {
+        if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
+          OpXRayRx rx{}; rx.v = v; rx.src = 3 + j; rx.j = j;
+          OpXRayRtv rt{}; rt.v = v; rt.src = 3 + j; rt.j = j;
+          AQP_CUDA(run_spmv(st, p->R, rx, gr));
+          AQP_CUDA(run_spmv(st, p->Rt, rt, gr));
+        }
+        OpChkXRayT<true> q{}; q.v = v; q.j = j; q.which = 1;
+        AQP_CUDA(run_spmv(st, p->Q, q, gr));
+      }
+    }
+  }
+  AQP_TRY(pull_ctrl(s));
+  const double *r = s->h.red;
+  aqp_check_result &o = *out;
+  std::memset(&o, 0, sizeof(o));
+  o.primal_viol = r[R_PV];
+  o.dual_viol = r[R_DV];
+  o.qx_inf = r[R_QXI];
+  o.aty_inf = r[R_ATYI];
+  o.pr_pos = r[R_PRP]; o.pr_neg = r[R_PRN]; o.pr_bad = (int32_t)r[R_PRB];
+  o.py_pos = r[R_PYP]; o.py_neg = r[R_PYN]; o.py_bad = (int32_t)r[R_PYB];
+  o.xqx = r[R_XQX];
+  o.cx = r[R_CX];
+  o.pid_dx2 = r[R_PIDX];
+  o.pid_dy2 = r[R_PIDY];
+  o.have_avg_prev = s->h.s.have_avg_prev;
+  for (int j = 0; j < 2; ++j) {
+    const double *y = r + R_YR + 9 * j;
+    o.yr_norm[j] = y[0]; o.yr_viol[j] = y[1]; o.yr_aty_inf[j] = y[2];
+    o.yr_var_pos[j] = y[3]; o.yr_var_neg[j] = y[4]; o.yr_var_bad[j] = (int32_t)y[5];
+    o.yr_con_pos[j] = y[6]; o.yr_con_neg[j] = y[7]; o.yr_con_bad[j] = (int32_t)y[8];
+    const double *x = r + R_XR + 5 * j;
+    o.xr_norm[j] = x[0]; o.xr_improvement[j] = x[1]; o.xr_viol_x[j] = x[2];
+    o.xr_viol_s[j] = x[3]; o.xr_qd_inf[j] = x[4];
+  }
+  if (rays) {
+    // engine.py:443-453: the window restarts and the averages become "previous"
+    s->h.s.block_len = 0;
+    s->h.s.have_avg_prev = 1;
+    AQP_TRY(push_scalars(s));
+  }
+  return AQP_OK;
+}
+
+int aqp_solver_mark_cert(aqp_solver *s) { return s ? state_op(s, 1) : fail(AQP_EINVAL, "NULL"); }
+int aqp_solver_restart(aqp_solver *s) { return s ? state_op(s, 2) : fail(AQP_EINVAL, "NULL"); }
+int aqp_solver_rollback(aqp_solver *s) { return s ? state_op(s, 3) : fail(AQP_EINVAL, "NULL"); }
+
+int aqp_solver_reset_window(aqp_solver *s) {
+  if (!s) return fail(AQP_EINVAL, "NULL");
+  AQP_TRY(state_op(s, 4));
+  return AQP_OK;
+}
+
+int aqp_solver_read(aqp_solver *s, int which, double *host_out, int64_t len) {
+  if (!s || !host_out) return fail(AQP_EINVAL, "NULL argument");
+  const SV &v = s->v;
+  const double *src = nullptr;
+  int64_t need = 0;
+  switch (which) {
+    case 0: src = v.xeval; need = s->p->n; break;
+    case 1: src = pick3(v.ys, s->h.ycur); need = s->p->m; break;
+    case 2: src = v.rs; need = s->p->n; break;
+    case 3: src = pick2(v.dy, 0); need = s->p->m; break;
+    case 4: src = pick2(v.dy, 1); need = s->p->m; break;
+    case 5: src = pick2(v.dx, 0); need = s->p->n; break;
+    case 6: src = pick2(v.dx, 1); need = s->p->n; break;
+    case 7: src = pick3(v.xs, s->h.xcur); need = s->p->n; break;
+    default: return fail(AQP_EINVAL, "unknown buffer id");
+  }
+  if (len != need) return fail(AQP_EINVAL, "length mismatch");
+  if (which == 1 || which == 7) {
+    AQP_TRY(pull_ctrl(s));
+    src = which == 1 ? pick3(v.ys, s->h.ycur) : pick3(v.xs, s->h.xcur);
+  }
+  cudaStream_t st = s->p->ctx->stream;
+  if (need) AQP_CUDA(cudaMemcpyAsync(host_out, src, need * 8, cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  return AQP_OK;
+}
+
+int aqp_solver_counters(aqp_solver *s, int64_t *out) {
+  if (!s || !out) return fail(AQP_EINVAL, "NULL argument");
+  out[0] = s->launches_per_iter_fixed;
+  out[1] = s->p->quad_kind == AQP_QUAD_DIAGONAL ? 0 : (s->p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK ? 4 : 2);
+  return AQP_OK;
+}
+
+// power iteration for the step size (linalg.py:287-312); runs before init
+int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, double *out, int *annihilated) {
+  if (!s || !host_v0 || !out || !annihilated) return fail(AQP_EINVAL, "NULL argument");
+  aqp_problem *p = s->p;
+  cudaStream_t st = p->ctx->stream;
+  const SV &v = s->v;
+  GridRed gr = s->gr;
+  const int64_t n = p->n;
+  *annihilated = 0;
+  AQP_TRY(poke(s, &Ctrl::pw_stop, 0));
+  AQP_CUDA(cudaMemcpyAsync(pick3(v.xbb, 0), host_v0, n * 8, cudaMemcpyHostToDevice, st));
+  // nv = |v|; u = v / nv; |A u| > 0 ?
+  { OpPwNorm o{}; o.v = v; o.idx = 0; o.slot = R_PW; AQP_CUDA(run_elem(st, n, o, gr)); }
+  { OpPwScale o{}; o.v = v; o.src = 0; o.dst = 1; o.slot = R_PW; AQP_CUDA(run_elem(st, n, o, gr)); }
+  { OpStoreT<false> a{}; a.v = v; a.src = 2; a.dst = 2; a.red = R_PW + 1; AQP_CUDA(run_spmv(st, p->A, a, gr)); }
+  AQP_TRY(pull_ctrl(s));
+  if (!(s->h.red[R_PW] > 0.0) || !(s->h.red[R_PW + 1] > 0.0)) {
+    *annihilated = 1;
+    return AQP_OK;
+  }
+  for (int it = 0; it < iters; ++it) {
+    OpStoreT<false> a{}; a.v = v; a.src = 2; a.dst = 2; a.red = -1;           // t = A v
+    AQP_CUDA(run_spmv(st, p->A, a, gr));
+    OpStoreT<false> b{}; b.v = v; b.src = 3; b.dst = 3; b.red = R_PW + 2;     // w = A't, |w|^2
+    AQP_CUDA(run_spmv(st, p->At, b, gr));
+    k_pw_check<<<1, 1, 0, st>>>(s->d_ctrl, R_PW + 2);
+    AQP_CUDA(cudaGetLastError());
+    OpPwScale c{}; c.v = v; c.src = 2; c.dst = 1; c.slot = R_PW + 2;          // v = w / |w|
+    AQP_CUDA(run_elem(st, n, c, gr));
+  }
+  // final |A v| (the stop flag must not suppress it)
+  AQP_TRY(poke(s, &Ctrl::pw_stop, 0));
+  { OpStoreT<false> a{}; a.v = v; a.src = 2; a.dst = 2; a.red = R_PW + 3; AQP_CUDA(run_spmv(st, p->A, a, gr)); }
+  AQP_TRY(pull_ctrl(s));
+  *out = sqrt(s->h.red[R_PW + 3]);
+  return AQP_OK;
+}
+
+}  // extern "C"

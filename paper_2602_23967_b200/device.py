@@ -1,0 +1,218 @@
+"""Device-side objects: PyTorch owns the HBM, libaqp owns the layout and math.
+
+* :class:`DeviceContext` binds libaqp to a CUDA device and a torch stream.
+* :class:`DeviceProblem` uploads a :class:`~.model.QpProblem` (reference
+  layouts: int64 CSR + float64) and lets libaqp build the device form -- int32
+  CSR of A, an explicit A' and the full symmetric Q, their SpMV work plans
+  and the cone codes -- inside one torch-allocated workspace.
+* :class:`DeviceSolver` is the iteration state of one ``solve`` call.
+
+Nothing here computes on the host; a missing library or device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as nat
+from .errors import DeviceError
+from .model import QpProblem
+
+_contexts = {}
+
+
+def _torch():
+    try:
+        import torch
+    except ImportError as exc:  # pragma: no cover - torch is part of the image
+        raise DeviceError("PyTorch is required for device buffers") from exc
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device available: the solver has no host fallback")
+    return torch
+
+
+class DeviceContext:
+    """libaqp context on (device, current torch stream)."""
+
+    def __init__(self, device: int = 0):
+        torch = _torch()
+        self.lib = nat.load()
+        self.device = int(device)
+        torch.cuda.set_device(self.device)
+        self.torch = torch
+        self.stream = torch.cuda.current_stream(self.device)
+        h = C.c_void_p()
+        nat.check(self.lib.aqp_ctx_create(self.device, C.c_void_p(self.stream.cuda_stream), C.byref(h)),
+                  "aqp_ctx_create")
+        self.handle = h
+
+    @classmethod
+    def get(cls, device: int = 0) -> "DeviceContext":
+        torch = _torch()
+        key = (int(device), torch.cuda.current_stream(int(device)).cuda_stream)
+        ctx = _contexts.get(key)
+        if ctx is None:
+            ctx = _contexts[key] = cls(device)
+        return ctx
+
+    def empty(self, nbytes: int):
+        return self.torch.empty(max(int(nbytes), 1), dtype=self.torch.uint8, device=f"cuda:{self.device}")
+
+    def upload(self, arr: np.ndarray):
+        return self.torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}", non_blocking=False)
+
+
+class DeviceProblem:
+    """HBM copy of one QpProblem (reference model.py:124-165)."""
+
+    def __init__(self, problem: QpProblem, ctx: DeviceContext = None):
+        self.ctx = ctx or DeviceContext.get()
+        lib = self.ctx.lib
+        p = problem
+        a = p.constraint_matrix
+        q = p.quad
+        keep = []  # upload tensors, alive until create() returns
+
+        def up(arr):
+            t = self.ctx.upload(arr)
+            keep.append(t)
+            return t.data_ptr()
+
+        d = nat.ProblemDesc()
+        d.n, d.m = p.n, p.m
+        d.a_indptr, d.a_indices, d.a_data, d.a_nnz = up(a.indptr), up(a.indices), up(a.data), a.nnz
+        host_q = host_r = None
+        if q.kind == "diagonal":
+            d.quad_kind = nat.QUAD_DIAGONAL
+            d.q_values = up(q.values)
+        else:
+            pq = q if q.kind == "sparse" else q.p
+            d.quad_kind = nat.QUAD_SPARSE if q.kind == "sparse" else nat.QUAD_SPARSE_LOW_RANK
+            d.q_indptr, d.q_indices, d.q_data = up(pq.upper.indptr), up(pq.upper.indices), up(pq.upper.data)
+            d.q_nnz = pq.upper.nnz
+            d.q_diag = up(pq.diag)
+            host_q = pq.upper.indptr
+            if q.kind == "sparse_low_rank":
+                r = q.r
+                d.r_rows = r.rows
+                d.r_indptr, d.r_indices, d.r_data, d.r_nnz = up(r.indptr), up(r.indices), up(r.data), r.nnz
+                host_r = r.indptr
+        d.cost, d.var_lo, d.var_hi = up(p.cost), up(p.var_bounds.lower), up(p.var_bounds.upper)
+        d.con_lo, d.con_hi = up(p.con_bounds.lower), up(p.con_bounds.upper)
+        pb, sb = C.c_size_t(), C.c_size_t()
+        nat.check(lib.aqp_problem_sizes(C.byref(d), C.byref(pb), C.byref(sb)), "aqp_problem_sizes")
+        self.workspace = self.ctx.empty(pb.value)
+        scratch = self.ctx.empty(sb.value)
+        h = C.c_void_p()
+        rc = lib.aqp_problem_create(
+            self.ctx.handle, C.byref(d), a.indptr.ctypes.data,
+            None if host_q is None else host_q.ctypes.data,
+            None if host_r is None else host_r.ctypes.data,
+            C.c_void_p(self.workspace.data_ptr()), pb.value, C.c_void_p(scratch.data_ptr()), sb.value, C.byref(h))
+        nat.check(rc, "aqp_problem_create")
+        del scratch, keep
+        self.handle = h
+        self.n, self.m = p.n, p.m
+        self.kind = q.kind
+        info = nat.ProblemInfo()
+        nat.check(lib.aqp_problem_get_info(h, C.byref(info)))
+        self.info = info
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.ctx.lib.aqp_problem_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceSolver:
+    """Iteration state of one solve (engine.py:125-155 plus the locals of solve)."""
+
+    X_EVAL, Y, DUAL_SLACK, YRAY0, YRAY1, XRAY0, XRAY1, X = range(8)
+
+    def __init__(self, prob: DeviceProblem, *, eps_tol, eps_inf, gamma_sys, tol_scale, tol_floor, diag_bound,
+                 adaptive, max_inner, halpern):
+        self.prob = prob
+        self.lib = prob.ctx.lib
+        prm = nat.SolverParamsC()
+        prm.eps_tol, prm.eps_inf, prm.gamma_sys = eps_tol, eps_inf, gamma_sys
+        prm.tol_scale, prm.tol_floor, prm.diag_bound = tol_scale, tol_floor, diag_bound
+        prm.adaptive, prm.max_inner, prm.halpern = int(adaptive), int(max_inner), int(halpern)
+        sz = C.c_size_t()
+        nat.check(self.lib.aqp_solver_sizes(prob.handle, C.byref(sz)), "aqp_solver_sizes")
+        self.workspace = prob.ctx.empty(sz.value)
+        h = C.c_void_p()
+        nat.check(self.lib.aqp_solver_create(prob.handle, C.byref(prm), C.c_void_p(self.workspace.data_ptr()),
+                                             sz.value, C.byref(h)), "aqp_solver_create")
+        self.handle = h
+        self.sc = nat.Scalars()
+
+    # -- scalars ----------------------------------------------------------
+    def init(self, sc: nat.Scalars):
+        nat.check(self.lib.aqp_solver_init(self.handle, C.byref(sc)), "aqp_solver_init")
+
+    def get_scalars(self) -> nat.Scalars:
+        sc = nat.Scalars()
+        nat.check(self.lib.aqp_solver_get_scalars(self.handle, C.byref(sc)), "aqp_solver_get_scalars")
+        return sc
+
+    def set_scalars(self, sc: nat.Scalars):
+        nat.check(self.lib.aqp_solver_set_scalars(self.handle, C.byref(sc)), "aqp_solver_set_scalars")
+
+    # -- work ----------------------------------------------------------------
+    def estimate_norm(self, v0: np.ndarray, iters: int):
+        v0 = np.ascontiguousarray(v0, dtype=np.float64)
+        out = C.c_double()
+        ann = C.c_int()
+        nat.check(self.lib.aqp_solver_estimate_norm(self.handle, v0.ctypes.data, int(iters), C.byref(out),
+                                                    C.byref(ann)), "aqp_solver_estimate_norm")
+        return out.value, bool(ann.value)
+
+    def run(self, n_iters: int):
+        nat.check(self.lib.aqp_solver_run(self.handle, int(n_iters)), "aqp_solver_run")
+
+    def check(self, with_rays: bool) -> nat.CheckResult:
+        cr = nat.CheckResult()
+        nat.check(self.lib.aqp_solver_check(self.handle, int(bool(with_rays)), C.byref(cr)), "aqp_solver_check")
+        return cr
+
+    def mark_cert(self):
+        nat.check(self.lib.aqp_solver_mark_cert(self.handle))
+
+    def restart(self):
+        nat.check(self.lib.aqp_solver_restart(self.handle))
+
+    def rollback(self):
+        nat.check(self.lib.aqp_solver_rollback(self.handle))
+
+    def reset_window(self):
+        nat.check(self.lib.aqp_solver_reset_window(self.handle))
+
+    def read(self, which: int) -> np.ndarray:
+        length = self.prob.m if which in (self.Y, self.YRAY0, self.YRAY1) else self.prob.n
+        out = np.empty(length, dtype=np.float64)
+        nat.check(self.lib.aqp_solver_read(self.handle, int(which), out.ctypes.data, length), "aqp_solver_read")
+        return out
+
+    def counters(self):
+        buf = (C.c_int64 * 2)()
+        nat.check(self.lib.aqp_solver_counters(self.handle, buf))
+        return int(buf[0]), int(buf[1])
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.aqp_solver_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

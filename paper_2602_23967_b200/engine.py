@@ -1,0 +1,358 @@
+"""The solve entry point: host control of the device-resident PDHCG-II loop.
+
+Drop-in for ``anchorqp.solve`` (reference ``anchorqp/engine.py:339-498``):
+same parameters, statuses, result object, progress-callback cadence and
+branch logic.  The iterations themselves never touch the host: each
+certification window (<= ``check_every`` outer iterations, each with its
+full BB inner solve) is ONE CUDA-graph launch of libaqp, and the host only
+synchronises at certification points to run the reference's decision chain
+(optimality, ray tests, stall probe, divergence rollback, restart + PID) on
+the device-computed scalars.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import enum
+import math
+import time
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _native as nat
+from . import certify
+from .certify import Certificate, CertificateKind, ResidualReport
+from .device import DeviceContext, DeviceProblem, DeviceSolver
+from .model import QpProblem, validate
+
+# engine.py:26-49
+OMEGA_MIN = 1e-6
+OMEGA_MAX = 1e6
+PID_INTEGRAL_CLAMP = 10.0
+ETA_UNCONSTRAINED = 1e8
+DIVERGENCE_FACTOR = 100.0
+THETA_BACKOFF_FLOOR = 1e-2
+STALL_CHECKS = 8
+STALL_IMPROVEMENT = 0.99
+PROBE_INNER_TOL = 1e-12  # applied on the device (OpGrad<true>::finalize)
+
+
+class SolveStatus(str, enum.Enum):
+    OPTIMAL = "optimal"
+    PRIMAL_INFEASIBLE = "primal_infeasible"
+    DUAL_INFEASIBLE = "dual_infeasible"
+    ITERATION_LIMIT = "iteration_limit"
+    TIME_LIMIT = "time_limit"
+
+
+@dataclasses.dataclass(frozen=True)
+class RestartParams:
+    """engine.py:60-74."""
+
+    beta_sufficient: float = 0.2
+    beta_necessary: float = 0.8
+    max_round_len: int = 2000
+    enabled: bool = True
+
+    def __post_init__(self):
+        if self.enabled and not 0.0 < self.beta_sufficient < self.beta_necessary < 1.0:
+            raise ValueError("restart betas must satisfy 0 < sufficient < necessary < 1")
+        if self.max_round_len < 1:
+            raise ValueError("max_round_len must be positive")
+
+
+@dataclasses.dataclass(frozen=True)
+class InnerParams:
+    """engine.py:77-86."""
+
+    adaptive: bool = True
+    initial: float = 1e-2
+    scale: float = 5e-4
+    floor: float = 1e-9
+    fixed_tol: float = 1e-9
+    max_inner: int = 200
+
+
+@dataclasses.dataclass(frozen=True)
+class SolverParams:
+    """engine.py:89-122 (defaults are the reference code's, not SPEC.md's)."""
+
+    eps_tol: float = 1e-6
+    eps_inf: float = 1e-9
+    theta: float = 0.0
+    eta_scale: float = 0.998
+    pid_gains: tuple = (0.5, 0.02, 0.1)
+    omega0: float = 1.0
+    restart: RestartParams = dataclasses.field(default_factory=RestartParams)
+    inner: InnerParams = dataclasses.field(default_factory=InnerParams)
+    iter_limit: int = 1_000_000
+    time_limit: Optional[float] = None
+    check_every: int = 64
+    halpern: bool = True
+    gamma_sys: Optional[float] = None
+    norm_iters: int = 100
+    norm_seed: int = 0
+
+    def __post_init__(self):
+        if self.eps_tol <= 0 or self.eps_inf <= 0:
+            raise ValueError("tolerances must be positive")
+        if not 0.0 <= self.theta < 1.0:
+            raise ValueError("theta must lie in [0, 1)")
+        if self.omega0 <= 0:
+            raise ValueError("omega0 must be positive")
+        if self.iter_limit < 1 or self.check_every < 1:
+            raise ValueError("iter_limit and check_every must be positive")
+        if self.time_limit is not None and self.time_limit <= 0:
+            raise ValueError("time_limit must be positive")
+
+
+@dataclasses.dataclass(frozen=True)
+class SolveResult:
+    """engine.py:157-171."""
+
+    status: SolveStatus
+    x: np.ndarray
+    y: np.ndarray
+    report: ResidualReport
+    certificate: Optional[Certificate]
+    outer_iterations: int
+    inner_iterations: int
+    restarts: int
+    seconds: float
+
+    @property
+    def rounds(self) -> int:
+        return self.restarts + 1
+
+
+ProgressCallback = Callable[[int, ResidualReport, float, int], None]
+
+
+@dataclasses.dataclass
+class _Round:
+    """Host-side scalars of SolverState (engine.py:125-146) that only change at
+    certification points; the per-iteration ones (k, inner tolerance) live in
+    the device control block."""
+
+    omega: float
+    eta: float
+    theta: float
+    round: int = 0
+    pid_integral: float = 0.0
+    pid_last_error: float = 0.0
+    best_residual_round_start: float = math.inf
+    last_check_kkt: float = math.inf
+
+
+def restart_decision(k: int, rs: _Round, kkt: float, params: SolverParams) -> bool:
+    """engine.py:248-257."""
+    if k >= params.restart.max_round_len:
+        return True
+    base = rs.best_residual_round_start
+    if kkt <= params.restart.beta_sufficient * base:
+        return True
+    if kkt <= params.restart.beta_necessary * base and kkt > rs.last_check_kkt:
+        return True
+    return False
+
+
+def pid_update(rs: _Round, dx: float, dy: float, params: SolverParams) -> float:
+    """engine.py:260-281 with |x - x_rs|, |y - y_rs| from the device."""
+    if dx <= 0.0 or dy <= 0.0 or not (math.isfinite(dx) and math.isfinite(dy)):
+        return rs.omega
+    error = math.log(rs.omega * dx / dy)
+    if not math.isfinite(error):
+        return rs.omega
+    kp, ki, kd = params.pid_gains
+    integral = min(max(rs.pid_integral + error, -PID_INTEGRAL_CLAMP), PID_INTEGRAL_CLAMP)
+    log_omega = math.log(rs.omega) - (kp * error + ki * integral + kd * (error - rs.pid_last_error))
+    rs.pid_integral = integral
+    rs.pid_last_error = error
+    return min(max(math.exp(log_omega), OMEGA_MIN), OMEGA_MAX)
+
+
+def estimate_eta(solver: DeviceSolver, problem: QpProblem, params: SolverParams) -> float:
+    """initialize()'s step scale (engine.py:178-183, linalg.py:287-312)."""
+    a = problem.constraint_matrix
+    if a.nnz == 0:
+        return ETA_UNCONSTRAINED
+    rng = np.random.default_rng(params.norm_seed)
+    for _ in range(8):
+        v = rng.standard_normal(a.cols)  # start vector drawn exactly as the reference draws it
+        est, annihilated = solver.estimate_norm(v, params.norm_iters)
+        if not annihilated:
+            return params.eta_scale / est
+    return ETA_UNCONSTRAINED
+
+
+class _Run:
+    """One solve: device objects + the reference's loop locals."""
+
+    def __init__(self, problem: QpProblem, params: SolverParams, progress, device: int):
+        self.problem = problem
+        self.params = params
+        self.progress = progress
+        ctx = DeviceContext.get(device)
+        self.dev = DeviceProblem(problem, ctx)
+        gamma = params.gamma_sys if params.gamma_sys is not None else certify.default_gamma_sys(problem)
+        self.gamma_sys = gamma
+        self.con_scale = certify.finite_bound_scale(problem.con_bounds)
+        self.cost_inf = certify.linf(problem.cost)
+        ip = params.inner
+        self.solver = DeviceSolver(
+            self.dev, eps_tol=params.eps_tol, eps_inf=params.eps_inf, gamma_sys=gamma,
+            tol_scale=ip.scale, tol_floor=ip.floor, diag_bound=problem.quad.diag_bound(),
+            adaptive=ip.adaptive, max_inner=ip.max_inner, halpern=params.halpern)
+
+    def report(self, cr, need_slack: bool) -> ResidualReport:
+        slack = self.solver.read(DeviceSolver.DUAL_SLACK) if need_slack else None
+        return certify.report_from_check(cr, self.con_scale, self.cost_inf, slack)
+
+
+def solve(problem, params: Optional[SolverParams] = None, progress: Optional[ProgressCallback] = None,
+          device: int = 0) -> SolveResult:
+    """Run until optimality, an infeasibility certificate, or a limit
+    (engine.py:339-498).  ``problem`` may be this package's QpProblem or the
+    reference's (rebuilt field by field)."""
+    params = params or SolverParams()
+    problem = QpProblem.from_any(problem)
+    validate(problem)
+    start = time.monotonic()
+    run = _Run(problem, params, progress, device)
+    sol = run.solver
+    rs = _Round(omega=params.omega0, eta=0.0, theta=params.theta)
+    rs.eta = estimate_eta(sol, problem, params)
+    tol0 = params.inner.initial if params.inner.adaptive else params.inner.fixed_tol
+    sc = nat.Scalars()
+    sc.eta, sc.omega, sc.theta, sc.inner_tol = rs.eta, rs.omega, rs.theta, tol0
+    sol.init(sc)
+
+    n_outer = n_inner = restarts = 0
+
+    def finish(status, report, cert):
+        x = sol.read(DeviceSolver.X_EVAL)
+        y = sol.read(DeviceSolver.Y)
+        if report.dual_slack is None:
+            report = dataclasses.replace(report, dual_slack=sol.read(DeviceSolver.DUAL_SLACK))
+        return SolveResult(status=status, x=x, y=y, report=report, certificate=cert,
+                           outer_iterations=n_outer, inner_iterations=n_inner, restarts=restarts,
+                           seconds=time.monotonic() - start)
+
+    cr = sol.check(with_rays=False)
+    report = run.report(cr, progress is not None)
+    rs.best_residual_round_start = report.kkt_max
+    rs.last_check_kkt = report.kkt_max
+    if progress is not None:
+        progress(0, report, rs.omega, rs.round)
+    if certify.check_optimal(report, params.eps_tol):
+        return finish(SolveStatus.OPTIMAL, report, None)
+    sol.mark_cert()
+    best_kkt_seen = report.kkt_max
+    stall_checks = 0
+    probe_until = 0
+    rp = params.restart
+    check_every = params.check_every
+
+    def push(**kw):
+        s = sol.get_scalars()
+        for k, v in kw.items():
+            setattr(s, k, v)
+        sol.set_scalars(s)
+        return s
+
+    def rollback_round():
+        # engine.py:303-319 (vectors on the device)
+        sol.rollback()
+        rs.round += 1
+        rs.theta = rs.theta / 2.0 if rs.theta >= THETA_BACKOFF_FLOOR else 0.0
+        rs.last_check_kkt = rs.best_residual_round_start
+        push(k=0, theta=rs.theta)
+
+    def reanchor(kkt):
+        # engine.py:322-333 (and the vector half of _do_restart)
+        sol.restart()
+        rs.round += 1
+        rs.best_residual_round_start = kkt
+        rs.last_check_kkt = kkt
+
+    while n_outer < params.iter_limit:
+        probing = n_outer < probe_until
+        sc = push(probing=int(probing))
+        window = check_every - (n_outer % check_every)
+        window = min(window, params.iter_limit - n_outer)
+        if probing:
+            window = min(window, probe_until - n_outer)
+        elif rp.enabled:
+            window = min(window, max(1, rp.max_round_len - sc.k))
+        sol.run(window)
+        sc = sol.get_scalars()
+        n_outer += sc.iters_done
+        n_inner += sc.inner_sum
+        if sc.halted:
+            # engine.py:407-417: overflow inside the round
+            sol.rollback()
+            rs.round += 1
+            rs.theta = rs.theta / 2.0 if rs.theta >= THETA_BACKOFF_FLOOR else 0.0
+            rs.last_check_kkt = rs.best_residual_round_start
+            sol.mark_cert()
+            probe_until = 0
+            sol.reset_window()
+            push(k=0, theta=rs.theta, halted=0, block_len=0, have_avg_prev=0)
+            continue
+        at_cap = (not probing) and rp.enabled and sc.k >= rp.max_round_len
+        if not (n_outer % check_every == 0 or at_cap or n_outer == params.iter_limit):
+            continue  # window ended at the probe boundary
+        # ---- certification point (engine.py:436-494) -----------------------
+        cr = sol.check(with_rays=True)
+        report = run.report(cr, progress is not None)
+        kkt = report.kkt_max
+        if progress is not None:
+            progress(n_outer, report, rs.omega, rs.round)
+        if certify.check_optimal(report, params.eps_tol):
+            return finish(SolveStatus.OPTIMAL, report, None)
+        order = (0, 1) if cr.have_avg_prev else (1,)
+        for j in order:
+            hit = certify.primal_ray_test(cr, j, params.eps_inf)
+            if hit is not None:
+                ray = sol.read(DeviceSolver.YRAY0 + j)
+                return finish(SolveStatus.PRIMAL_INFEASIBLE, report,
+                              Certificate(CertificateKind.PRIMAL_RAY, ray, hit[0], hit[1]))
+        for j in order:
+            hit = certify.dual_ray_test(cr, j, params.eps_tol, params.eps_inf, run.gamma_sys)
+            if hit is not None:
+                ray = sol.read(DeviceSolver.XRAY0 + j)
+                return finish(SolveStatus.DUAL_INFEASIBLE, report,
+                              Certificate(CertificateKind.DUAL_RAY, ray, hit[0], hit[1]))
+        sol.mark_cert()
+        if math.isfinite(kkt) and kkt < STALL_IMPROVEMENT * best_kkt_seen:
+            best_kkt_seen = min(best_kkt_seen, kkt)
+            stall_checks = 0
+        else:
+            stall_checks += 1
+        k_now = sol.get_scalars().k
+        if probing:
+            if n_outer >= probe_until:
+                if stall_checks == 0:
+                    reanchor(kkt)
+                    push(k=0)
+                else:
+                    probe_until = n_outer + rp.max_round_len
+        elif stall_checks >= STALL_CHECKS:
+            probe_until = n_outer + rp.max_round_len
+        elif not math.isfinite(kkt) or kkt > DIVERGENCE_FACTOR * rs.best_residual_round_start:
+            rollback_round()
+            sol.mark_cert()
+        elif rp.enabled and restart_decision(k_now, rs, kkt, params):
+            if kkt < rs.best_residual_round_start:  # anti-windup, engine.py:284-290
+                rs.omega = pid_update(rs, math.sqrt(cr.pid_dx2), math.sqrt(cr.pid_dy2), params)
+            reanchor(kkt)
+            restarts += 1
+            push(k=0, omega=rs.omega)
+        else:
+            rs.last_check_kkt = kkt
+        if params.time_limit is not None and time.monotonic() - start >= params.time_limit:
+            return finish(SolveStatus.TIME_LIMIT, report, None)
+
+    cr = sol.check(with_rays=False)
+    return finish(SolveStatus.ITERATION_LIMIT, run.report(cr, False), None)
