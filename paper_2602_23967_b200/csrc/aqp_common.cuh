@@ -55,6 +55,18 @@ __host__ __device__ __forceinline__ double clip(double v, double lo, double hi) 
 __host__ __device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
 __host__ __device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
 
+// |x| by clearing the sign bit.  nvcc 12.9 -O3 miscompiles
+// nanmax(0.0, fabs(d)) into `d > 0 ? |d| : 0` (SASS: DSETP.GTU on the
+// un-abs'd operand), silently dropping negative residual components from
+// every inf-norm (it also sees through a sign-bit mask).  An empty asm
+// barrier makes the magnitude opaque, so no compare-with-zero rewrite can
+// reach back to the signed operand.
+__device__ __forceinline__ double absd(double x) {
+  double r = fabs(x);
+  asm volatile("" : "+d"(r));
+  return r;
+}
+
 // numpy.max over nonnegative values with NaN propagation (np.abs(v).max())
 __device__ __forceinline__ double nanmax(double a, double b) {
   if (a != a) return a;

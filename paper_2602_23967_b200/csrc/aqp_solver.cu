@@ -273,7 +273,7 @@ struct OpGrad {
       const bool conv = res <= ct->target;
       if (conv || t_ >= v.max_inner) {
         // return rule, inner.py:129-134
-        const double noise = 64.0 * 2.220446049250313e-16 * (1.0 + fabs(ct->best_phi));
+        const double noise = 64.0 * 2.220446049250313e-16 * (1.0 + absd(ct->best_phi));
         if ((conv && phi <= ct->best_phi + noise) || phi <= ct->best_phi)
           ct->bb_xplus = ct->bb_cur;
         else
@@ -448,13 +448,13 @@ struct OpChkX {
       if (have_prev) {
         const double d0 = avg - v.xavgp[i];
         pick2(v.dx, 0)[i] = d0;
-        acc.m[0] = nanmax(acc.m[0], fabs(d0));
+        acc.m[0] = nanmax(acc.m[0], absd(d0));
       }
       v.xavgp[i] = avg;
       v.xblk[i] = 0.0;
       const double d1 = xi - v.xlast[i];
       pick2(v.dx, 1)[i] = d1;
-      acc.m[1] = nanmax(acc.m[1], fabs(d1));
+      acc.m[1] = nanmax(acc.m[1], absd(d1));
     }
   }
   __device__ void finalize(const RedVals<1, 2> &t) const {
@@ -494,13 +494,13 @@ struct OpChkY {
       if (have_prev) {
         const double p0 = cone_proj(avg - v.yavgp[i], cy);
         pick2(v.dy, 0)[i] = p0;
-        acc.m[0] = nanmax(acc.m[0], fabs(p0));
+        acc.m[0] = nanmax(acc.m[0], absd(p0));
       }
       v.yavgp[i] = avg;
       v.yblk[i] = 0.0;
       const double p1 = cone_proj(yi - v.ylast[i], cy);
       pick2(v.dy, 1)[i] = p1;
-      acc.m[1] = nanmax(acc.m[1], fabs(p1));
+      acc.m[1] = nanmax(acc.m[1], absd(p1));
     }
   }
   __device__ void finalize(const RedVals<4, 2> &t) const {
@@ -533,7 +533,7 @@ struct OpChkA {
   }
   __device__ double gather(int c) const { return __ldg(v.xeval + c); }
   __device__ void row(int r, double s, RedVals<6, 1> &acc) const {
-    acc.m[0] = nanmax(acc.m[0], fabs(s - clip(s, v.clo[r], v.chi[r])));
+    acc.m[0] = nanmax(acc.m[0], absd(s - clip(s, v.clo[r], v.chi[r])));
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       if (!ok[j]) continue;
@@ -616,9 +616,9 @@ struct OpChkR {
     const double r = (q + c) + at;
     v.rs[i] = r;
     const double rp = cone_proj(r, v.cone_r[i]);
-    acc.m[0] = nanmax(acc.m[0], fabs(r - rp));
-    acc.m[1] = nanmax(acc.m[1], fabs(q));
-    acc.m[2] = nanmax(acc.m[2], fabs(at));
+    acc.m[0] = nanmax(acc.m[0], absd(r - rp));
+    acc.m[1] = nanmax(acc.m[1], absd(q));
+    acc.m[2] = nanmax(acc.m[2], absd(at));
     double bad = acc.s[2];
     support_add(-rp, v.vlo[i], v.vhi[i], acc.s[0], acc.s[1], bad);
     acc.s[2] = bad;
@@ -630,7 +630,7 @@ struct OpChkR {
       const double d = pick2(v.dx, j)[i] / nrm[j];
       pick2(v.dx, j)[i] = d;
       acc.s[5 + j] += c * d;
-      acc.m[3 + j] = nanmax(acc.m[3 + j], fabs(d - cone_proj(d, v.recc_x[i])));
+      acc.m[3 + j] = nanmax(acc.m[3 + j], absd(d - cone_proj(d, v.recc_x[i])));
     }
   }
   __device__ void finalize(const RedVals<7, 5> &t) const {
@@ -665,8 +665,8 @@ struct OpChkYRay {
   __device__ double gather(int c) const { return __ldg(ray + c); }
   __device__ void row(int r, double s, RedVals<3, 2> &acc) const {
     const double p = cone_proj(s, v.cone_r[r]);
-    acc.m[0] = nanmax(acc.m[0], fabs(s - p));
-    acc.m[1] = nanmax(acc.m[1], fabs(s));
+    acc.m[0] = nanmax(acc.m[0], absd(s - p));
+    acc.m[1] = nanmax(acc.m[1], absd(s));
     double bad = acc.s[2];
     support_add(-p, v.vlo[r], v.vhi[r], acc.s[0], acc.s[1], bad);
     acc.s[2] = bad;
@@ -698,13 +698,13 @@ struct OpChkXRay {
   __device__ double gather(int c) const { return __ldg(d + c); }
   __device__ void row(int r, double s, RedVals<0, 1> &acc) const {
     if (which == 0) {
-      acc.m[0] = nanmax(acc.m[0], fabs(s - cone_proj(s, v.recc_s[r])));
+      acc.m[0] = nanmax(acc.m[0], absd(s - cone_proj(s, v.recc_s[r])));
     } else {
-      acc.m[0] = nanmax(acc.m[0], fabs(quad_row(v, r, s)));
+      acc.m[0] = nanmax(acc.m[0], absd(quad_row(v, r, s)));
     }
   }
   __device__ void elem(int64_t i, RedVals<0, 1> &acc) const {  // diagonal Q: |q_i d_i|
-    acc.m[0] = nanmax(acc.m[0], fabs(v.qd[i] * d[i]));
+    acc.m[0] = nanmax(acc.m[0], absd(v.qd[i] * d[i]));
   }
   __device__ void finalize(const RedVals<0, 1> &t) const {
     v.ctrl->red[R_XR + 5 * j + 3 + which] = t.m[0];
