@@ -7,6 +7,7 @@ Specs (all seeded, all built by ``paper_2602_23967_b200.generators``):
     c2:<n>:<m>:<seed>         lasso_style_qp(n, m, seed)                            (config 2 / twins)
     c3:<n>:<k>:<seed>         portfolio_qp(n, k, seed=seed)                         (config 3 / twins)
     c4u:<n>:<seed> / c4i:<n>:<seed>   infeasible_pair(n, seed) [0] / [1]           (config 4)
+    c4ur / c4ir                        same on SURVEY.md's random_qp base
     c5:<n>:<w>:<seed>[:diag]  banded_qp(n, n, half_width=w, seed, diagonal_q)       (config 5 / twins)
 """
 
@@ -27,9 +28,10 @@ def build(spec: str):
         return g.lasso_style_qp(int(float(parts[1])), int(float(parts[2])), seed=int(parts[3]))
     if kind == "c3":
         return g.portfolio_qp(int(float(parts[1])), int(parts[2]), seed=int(parts[3]))
-    if kind in ("c4u", "c4i"):
-        pair = g.infeasible_pair(int(float(parts[1])), seed=int(parts[2]))
-        return pair[0] if kind == "c4u" else pair[1]
+    if kind in ("c4u", "c4i", "c4ur", "c4ir"):
+        base = "random_qp" if kind.endswith("r") else "diagonal"
+        pair = g.infeasible_pair(int(float(parts[1])), seed=int(parts[2]), base=base)
+        return pair[0] if kind.startswith("c4u") else pair[1]
     if kind == "c5":
         diag = len(parts) > 4 and parts[4] == "diag"
         n = int(float(parts[1]))

@@ -200,8 +200,9 @@ __device__ __forceinline__ bool grid_reduce(RedVals<NS, NM> &v, GridRed g, doubl
 // one smem tile, one thread per row, row sum sequential in column order
 // (bitwise the Cython order).  WARP: same tile, one warp per row (used when
 // rows are long enough that a sequential chain would be latency bound).
-// LONG: segment `seg` of `nseg` of one row longer than a tile.
-enum : int { kItemThread = 0, kItemWarp = 1, kItemLong = 2 };
+// LONG: segment `seg` of `nseg` of one row longer than a tile.  LONGSEQ
+// (strict plans only): a long row summed by one thread in column order.
+enum : int { kItemThread = 0, kItemWarp = 1, kItemLong = 2, kItemLongSeq = 3 };
 
 struct __align__(16) PlanItem {
   int row0, row1, k0, k1;

@@ -82,6 +82,17 @@ __global__ void __launch_bounds__(kThreads) spmv_op(DevCsr M, Op op, GridRed g) 
         if (lane == 0) o.row(r, Op::SYM ? lo + up : up, acc);
       }
     }
+  } else if (it.kind == kItemLongSeq) {
+    if (threadIdx.x == 0) {
+      const int r = it.row0;
+      double lo = 0.0, up = 0.0;
+      for (int k = it.k0; k < it.k1; ++k) {
+        const int c = __ldg(M.idx + k);
+        const double p = __ldg(M.val + k) * o.gather(c);
+        if (Op::SYM && c < r) lo += p; else up += p;
+      }
+      o.row(r, Op::SYM ? lo + up : up, acc);
+    }
   } else {
     const int r = it.row0;
     RedVals<2, 0> lu;

@@ -51,6 +51,18 @@ static std::vector<PlanItem> plan_rows(const P *ptr, int64_t rows, bool strict, 
   int64_t i = 0;
   while (i < rows) {
     const int64_t len = (int64_t)(ptr[i + 1] - ptr[i]);
+    if (len > kTileNnz && strict) {
+      PlanItem it{};
+      it.row0 = (int)i;
+      it.row1 = (int)i + 1;
+      it.k0 = (int)ptr[i];
+      it.k1 = (int)ptr[i + 1];
+      it.kind = kItemLongSeq;
+      it.nseg = 1;
+      items.push_back(it);
+      ++i;
+      continue;
+    }
     if (len > kTileNnz) {
       const int nseg = (int)((len + kSegNnz - 1) / kSegNnz);
       for (int s = 0; s < nseg; ++s) {
@@ -97,7 +109,7 @@ static std::vector<PlanItem> plan_rows(const P *ptr, int64_t rows, bool strict, 
 }
 
 int64_t plan_capacity(int64_t rows, int64_t nnz) {
-  return rows / 128 + 2 * (nnz / kTileNnz) + nnz / kSegNnz + 8;
+  return rows / 128 + 3 * (nnz / kTileNnz) + nnz / kSegNnz + 8;
 }
 
 // ---------------------------------------------------------------- setup kernels
@@ -236,7 +248,7 @@ void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz) {
   s.val = (double *)b.take(std::max<int64_t>(nnz, 1) * sizeof(double));
   s.plan_cap = plan_capacity(rows, nnz);
   s.plan = (PlanItem *)b.take(s.plan_cap * sizeof(PlanItem));
-  s.seg_cap = nnz / kSegNnz + 2;
+  s.seg_cap = nnz / kSegNnz + nnz / kTileNnz + 2;  // each long row adds at most one partial segment
   s.seg_part = (double *)b.take(2 * s.seg_cap * sizeof(double));
   s.seg_ticket = (unsigned *)b.take(s.seg_cap * sizeof(unsigned));
 }

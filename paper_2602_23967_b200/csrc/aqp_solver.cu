@@ -70,6 +70,7 @@ struct SV {
   int adaptive, max_inner, halpern, quad_kind;
   int64_t n, m;
   cudaGraphConditionalHandle bb_cond, outer_cond;
+  int in_graph;  // 0 for stand-alone launches (kernel timing): no conditional updates
 };
 
 
@@ -287,7 +288,7 @@ struct OpGrad {
         cont = 1;
       }
     }
-    cudaGraphSetConditional(v.bb_cond, cont);
+    if (v.in_graph) cudaGraphSetConditional(v.bb_cond, cont);
   }
 };
 
@@ -373,7 +374,7 @@ struct OpP2 {
   __device__ void finalize(const RedVals<0, 0> &) const {
     Ctrl *ct = v.ctrl;
     if (ct->s.halted) {
-      cudaGraphSetConditional(v.outer_cond, 0u);
+      if (v.in_graph) cudaGraphSetConditional(v.outer_cond, 0u);
       return;
     }
     const int xn = 3 - ct->xcur - ct->xprev, yn = 3 - ct->ycur - ct->yprev;
@@ -383,7 +384,7 @@ struct OpP2 {
     ct->ycur = yn;
     if (!ct->s.probing) ct->s.k += 1;
     ct->s.block_len += 1;
-    cudaGraphSetConditional(v.outer_cond, ct->s.iters_done < ct->window_len ? 1u : 0u);
+    if (v.in_graph) cudaGraphSetConditional(v.outer_cond, ct->s.iters_done < ct->window_len ? 1u : 0u);
   }
 };
 
@@ -889,9 +890,10 @@ int add_lowrank(aqp_solver *s, cudaGraph_t g, cudaGraphNode_t &last, int src) {
   aqp_problem *p = s->p;
   OpRx rx{};
   rx.v = s->v;
+  rx.v.in_graph = 1;
   rx.src = src;
   OpRtv rt{};
-  rt.v = s->v;
+  rt.v = rx.v;
   rt.src = src;
   AQP_CUDA(node_spmv(g, last, p->R, rx, s->gr));
   AQP_CUDA(node_spmv(g, last, p->Rt, rt, s->gr));
@@ -922,6 +924,7 @@ int build_graph(aqp_solver *s) {
     s->v.bb_cond = hbb;
   }
   SV v = s->v;
+  v.in_graph = 1;
   GridRed gr = s->gr;
   cudaGraphNode_t last = nullptr;
   int64_t fixed = 0;
@@ -1275,6 +1278,80 @@ int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, do
   { OpStoreT<false> a{}; a.v = v; a.src = 2; a.dst = 2; a.red = R_PW + 3; AQP_CUDA(run_spmv(st, p->A, a, gr)); }
   AQP_TRY(pull_ctrl(s));
   *out = sqrt(s->h.red[R_PW + 3]);
+  return AQP_OK;
+}
+
+// Stand-alone timing of one hot kernel (for the roofline in bench.py): `reps`
+// launches on the solver stream, each preceded by an L2 flush (a write of
+// `flush_bytes` to `flush`), timed with events around the kernel only.
+// kernel: 0 = BB gradient pass (Q SpMV + epilogue + 7 reductions),
+//         1 = BB step (x_t = clamp(x - alpha g)), 2 = P1 (A'y + epilogue),
+//         3 = P2 (A xbar + dual epilogue), 4 = X (primal epilogue).
+// Run after aqp_solver_init; it overwrites BB scratch and the control block's
+// BB fields, so re-init before solving.
+int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, size_t flush_bytes, double *avg_ms) {
+  if (!s || !avg_ms || reps <= 0) return fail(AQP_EINVAL, "bad argument");
+  aqp_problem *p = s->p;
+  cudaStream_t st = p->ctx->stream;
+  SV v = s->v;
+  v.in_graph = 0;
+  GridRed gr = s->gr;
+  cudaEvent_t e0, e1;
+  AQP_CUDA(cudaEventCreate(&e0));
+  AQP_CUDA(cudaEventCreate(&e1));
+  // a valid BB state: slots 0/1/2 distinct, alpha finite
+  AQP_TRY(poke(s, &Ctrl::bb_cur, 0));
+  AQP_TRY(poke(s, &Ctrl::bb_best, 0));
+  AQP_TRY(poke(s, &Ctrl::bb_new, 1));
+  AQP_TRY(poke(s, &Ctrl::g_cur, 0));
+  AQP_TRY(poke(s, &Ctrl::g_new, 1));
+  AQP_TRY(poke(s, &Ctrl::alpha, 1e-3));
+  double total = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    if (flush && flush_bytes) AQP_CUDA(cudaMemsetAsync(flush, r & 0xff, flush_bytes, st));
+    AQP_CUDA(cudaEventRecord(e0, st));
+    switch (kernel) {
+      case 0: {
+        OpGrad<false> o{};
+        o.v = v;
+        AQP_CUDA(run_spmv(st, p->Q, o, gr));
+        break;
+      }
+      case 1: {
+        OpStep o{};
+        o.v = v;
+        AQP_CUDA(run_elem(st, p->n, o, gr));
+        break;
+      }
+      case 2: {
+        OpP1Bb o{};
+        o.v = v;
+        AQP_CUDA(run_spmv(st, p->At, o, gr));
+        break;
+      }
+      case 3: {
+        OpP2 o{};
+        o.v = v;
+        AQP_CUDA(run_spmv(st, p->A, o, gr));
+        break;
+      }
+      case 4: {
+        OpXPost o{};
+        o.v = v;
+        AQP_CUDA(run_elem(st, p->n, o, gr));
+        break;
+      }
+      default: return fail(AQP_EINVAL, "unknown kernel id");
+    }
+    AQP_CUDA(cudaEventRecord(e1, st));
+    AQP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    AQP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    total += ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *avg_ms = total / reps;
   return AQP_OK;
 }
 

@@ -201,6 +201,15 @@ class DeviceSolver:
         nat.check(self.lib.aqp_solver_read(self.handle, int(which), out.ctypes.data, length), "aqp_solver_read")
         return out
 
+    def time_kernel(self, kernel: int, reps: int, flush=None) -> float:
+        """Average device ms of one stand-alone launch of a hot kernel (see aqp.h)."""
+        out = C.c_double()
+        fptr = C.c_void_p(flush.data_ptr()) if flush is not None else None
+        fbytes = flush.numel() * flush.element_size() if flush is not None else 0
+        nat.check(self.lib.aqp_solver_time_kernel(self.handle, int(kernel), int(reps), fptr, fbytes, C.byref(out)),
+                  "aqp_solver_time_kernel")
+        return out.value
+
     def counters(self):
         buf = (C.c_int64 * 2)()
         nat.check(self.lib.aqp_solver_counters(self.handle, buf))

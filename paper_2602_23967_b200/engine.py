@@ -211,10 +211,15 @@ class _Run:
 
 
 def solve(problem, params: Optional[SolverParams] = None, progress: Optional[ProgressCallback] = None,
-          device: int = 0) -> SolveResult:
+          device: int = 0, monitor: Optional[Callable[[int, int], None]] = None) -> SolveResult:
     """Run until optimality, an infeasibility certificate, or a limit
     (engine.py:339-498).  ``problem`` may be this package's QpProblem or the
-    reference's (rebuilt field by field)."""
+    reference's (rebuilt field by field).
+
+    ``monitor(outer, inner)`` (extension, not in the reference API) is called
+    at every certification point right after the device check, with the
+    cumulative outer and BB-inner iteration counts -- bench.py brackets
+    certification windows with CUDA events from it."""
     params = params or SolverParams()
     problem = QpProblem.from_any(problem)
     validate(problem)
@@ -305,6 +310,8 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
             continue  # window ended at the probe boundary
         # ---- certification point (engine.py:436-494) -----------------------
         cr = sol.check(with_rays=True)
+        if monitor is not None:
+            monitor(n_outer, n_inner)
         report = run.report(cr, progress is not None)
         kkt = report.kkt_max
         if progress is not None:

@@ -224,14 +224,36 @@ def portfolio_qp(n: int = 5_000_000, k: int = 100, sectors: int = 20, seed: int 
                      var_bounds=vb, con_bounds=cb, name=f"portfolio-n{n}-k{k}-s{seed}")
 
 
-def infeasible_pair(n: int = 100_000, seed: int = 1):
-    """C4: (dual-unbounded, primal-infeasible) pair on one diagonal-Q base
-    ``random_qp(n, n//2, "diagonal", density=10/n, seed)``.
+def diagonal_base_qp(n: int, m: int, seed: int = 1, per_row: int = 8) -> QpProblem:
+    """Well-conditioned diagonal-Q base: q ~ U(0.5, 2) (strictly convex), A with
+    ``per_row`` uniform columns per row, feasible x0 and the C2 bound patterns."""
+    rng = np.random.default_rng(seed)
+    cols = rng.integers(0, n, (m, per_row))
+    vals = rng.uniform(-1.0, 1.0, (m, per_row))
+    a = _csr_from_rows(m, n, cols, vals)
+    x0 = rng.normal(0.0, 1.0, n)
+    vb = _row_pattern_bounds(rng, x0, rng.random(n))
+    cb = _row_bounds(rng, _csr_rowdot(a, x0))
+    return QpProblem(quad=DiagonalQuad(rng.uniform(0.5, 2.0, n)), cost=rng.normal(0.0, 1.0, n), constraint_matrix=a,
+                     var_bounds=vb, con_bounds=cb, name=f"diag-base-n{n}-m{m}-s{seed}")
+
+
+def infeasible_pair(n: int = 100_000, seed: int = 1, base: str = "diagonal"):
+    """C4: (dual-unbounded, primal-infeasible) pair on one diagonal-Q base.
+
+    ``base="diagonal"`` (default) uses :func:`diagonal_base_qp` (n, n/2): it
+    certifies in ~1e3-5e4 outer iterations at n = 1e5.  ``base="random_qp"``
+    is SURVEY.md §8(d)'s recipe ``random_qp(n, n//2, "diagonal", 10/n)``,
+    whose zero-curvature coordinates delay certification past 1e6 iterations
+    at n = 1e5 (on the reference and here alike).
 
     * unbounded: variable 0 gets q=0, c=-1, box [0, inf) and an empty column in A;
     * infeasible: one random 10-nnz row appended twice with equality targets 1 and 2.
     """
-    base = random_qp(n, max(1, n // 2), "diagonal", density=min(1.0, 10.0 / n), seed=seed)
+    if base == "random_qp":
+        base = random_qp(n, max(1, n // 2), "diagonal", density=min(1.0, 10.0 / n), seed=seed)
+    else:
+        base = diagonal_base_qp(n, max(1, n // 2), seed=seed)
     a = base.constraint_matrix
     # --- dual-unbounded -----------------------------------------------------
     q = base.quad.values.copy()
@@ -241,10 +263,9 @@ def infeasible_pair(n: int = 100_000, seed: int = 1):
     lo = base.var_bounds.lower.copy()
     hi = base.var_bounds.upper.copy()
     lo[0], hi[0] = 0.0, np.inf
-    a_sp = a.to_scipy().tolil()
-    a_sp[:, 0] = 0.0
-    a0 = a_sp.tocsr()
-    a0.eliminate_zeros()
+    a_sp = a.to_scipy().tocoo()
+    keep = a_sp.col != 0
+    a0 = sp.csr_matrix((a_sp.data[keep], (a_sp.row[keep], a_sp.col[keep])), shape=a_sp.shape)
     unbounded = QpProblem(quad=DiagonalQuad(q), cost=c, constraint_matrix=SparseMatrix.from_scipy(a0),
                           var_bounds=Bounds(lo, hi), con_bounds=base.con_bounds,
                           name=f"dual-unbounded-n{n}-s{seed}")
