@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kThreads) spmv_op(DevCsr M, Op op, GridRed g) 
   RedVals<NS, NM> acc;
   acc.zero();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (it.kind != kItemLong) {
+  if (it.kind == kItemThread || it.kind == kItemWarp) {
     const int k0 = it.k0, k1 = it.k1;
 #pragma unroll 4
     for (int k = k0 + threadIdx.x; k < k1; k += kThreads) {
