@@ -41,6 +41,7 @@ constexpr int kThreads = 256;          // every kernel of the library uses 256-t
 constexpr int kWarps = kThreads / 32;
 constexpr int kTileNnz = 2048;         // nonzeros staged per SpMV row-block (16 KB + 8 KB smem)
 constexpr int kSegNnz = 8192;          // nonzeros per block for a split long row
+constexpr int kThreadRowMax = 48;      // longest row handled one-thread-per-row
 constexpr int kMaxRed = 16;            // max reduction slots of one kernel
 
 // ---------------------------------------------------------------- scalar helpers
@@ -149,51 +150,11 @@ __device__ __forceinline__ void block_reduce(RedVals<NS, NM> &v, double *smem /*
   __syncthreads();
 }
 
-// Grid-level epilogue shared by every reducing kernel: each block publishes
-// its partials; the last block to arrive (integer atomic ticket -- the
-// ticket order does not affect the arithmetic) folds all partials in block
-// order and returns true in thread 0 with the grid totals in `v`.
+// Grid-level epilogue: see grid_end / fin_op in aqp_kernels.cuh.
 struct GridRed {
-  double *partials;     // >= gridDim.x * (NS+NM) doubles
+  double *partials;     // >= kMaxRed * gridDim.x doubles, layout [slot][block]
   unsigned int *ticket;  // zero between launches (reset by the last block)
 };
-
-template <int NS, int NM>
-__device__ __forceinline__ bool grid_reduce(RedVals<NS, NM> &v, GridRed g, double *smem) {
-  constexpr int NT = NS + NM;
-  __shared__ bool last;
-  if constexpr (NT > 0) {
-    block_reduce<NS, NM>(v, smem);
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int i = 0; i < NS; ++i) g.partials[(size_t)blockIdx.x * NT + i] = v.s[i];
-#pragma unroll
-      for (int i = 0; i < NM; ++i) g.partials[(size_t)blockIdx.x * NT + NS + i] = v.m[i];
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(g.ticket, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!last) return false;
-  __threadfence();
-  if constexpr (NT > 0) {
-    // thread t folds blocks t, t+256, ... sequentially, then the fixed tree
-    RedVals<NS, NM> a;
-    a.zero();
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += kThreads) {
-      const double *p = g.partials + (size_t)b * NT;
-#pragma unroll
-      for (int i = 0; i < NS; ++i) a.s[i] += __ldcg(p + i);
-#pragma unroll
-      for (int i = 0; i < NM; ++i) a.m[i] = nanmax(a.m[i], __ldcg(p + NS + i));
-    }
-    block_reduce<NS, NM>(a, smem);
-    v = a;
-  }
-  if (threadIdx.x == 0) *g.ticket = 0u;
-  return threadIdx.x == 0;
-}
 
 // ---------------------------------------------------------------- SpMV work partition
 // One block per item.  THREAD: rows [row0,row1) whose nonzeros [k0,k1) fit
@@ -221,6 +182,8 @@ struct DevCsr {
   int nlongseg = 0;
   double *seg_part = nullptr;          // 2 * nlongseg doubles
   unsigned int *seg_ticket = nullptr;  // nlongseg counters
+  int smem_bytes = 0;                  // dynamic shared memory per block (WARP items only)
+  int uniform = 0;                     // every item is THREAD over rows [256 b, 256 b + 256)
 };
 
 }  // namespace aqp

@@ -1,11 +1,29 @@
-// aqp_kernels.cuh -- the two kernel skeletons every hot op of libaqp is built from.
+// aqp_kernels.cuh -- the kernel skeletons every op of libaqp is built from.
 //
 //   spmv_op<Op>: one pass over a CSR matrix (A, A', the full symmetric Q or
 //     P) with the op's per-row epilogue fused in and up to kMaxRed
-//     deterministic grid reductions finished by the last block (which then
-//     runs the op's scalar `finalize`, e.g. the BB step-size update).
-//   elem_op<Op>: one fixed-grid pass over a vector index space with the
-//     same reduction/finalize tail.
+//     deterministic reductions.
+//   elem_op<Op>: one fixed-grid pass over a vector index space, same tail.
+//   fin_op<Op>:  a single block that folds the partials of the preceding
+//     spmv_op/elem_op launch and runs the op's scalar `finalize` (e.g. the
+//     BB step-size rule and the CUDA-graph loop condition).
+//
+// Reductions end in one of two ways.  Hot ops (Op::SPLIT = true: the BB
+// gradient pass, the primal/dual epilogues) only publish per-block partials
+// and leave the fold to a fin_op node that follows in the graph -- measured on
+// C2, a last-block ticket (fence + atomic before every block retires) costs
+// ~14 us per launch, a one-block fin kernel ~3 us.  Cold ops (the
+// certification kernels) keep the last-block ticket.
+//
+// Row work of an SpMV is cut into plan items (aqp_problem.cu):
+//   THREAD  <= 256 short rows, one thread per row, the row's nonzeros read
+//           straight from HBM in column order (bitwise the Cython order);
+//           the row's epilogue operands are loaded first (Op::RowIn) so their
+//           latency overlaps the index -> gather chain;
+//   WARP    rows of medium length staged in shared memory, one warp per row;
+//   LONG    one segment of a row longer than a tile (block reduction, the
+//           last segment block combines the row);
+//   LONGSEQ (strict plans) a long row summed sequentially by one thread.
 //
 // Op concept:
 //   static constexpr int NS, NM;       number of sums / NaN-propagating maxes
@@ -13,74 +31,182 @@
 //                                      is (sum of j<r entries) + (sum of j>=r),
 //                                      each sequential -- bitwise the order of
 //                                      _core.pyx:62-80 sym_matvec
-//   static constexpr bool FINAL;       run finalize() in the last block
+//   static constexpr bool FINAL;       run finalize() after the grid is done
+//   [static constexpr bool SPLIT;]     finalize in a separate fin_op launch
 //   bool skip() const;                 uniform early exit (e.g. halted window)
 //   void prepare();                    per-thread setup on a private copy of the
 //                                      op (resolves device-side slot indices)
 //   double gather(int col) const;      (spmv) source vector entry
 //   void row(int r, double v, RedVals&) const;   (spmv) epilogue for row r
+//   [struct RowIn; RowIn load_row(int r) const;
+//    void row_in(int r, double v, const RowIn&, RedVals&) const;]
 //   void elem(int64_t i, RedVals&) const;        (elem)
-//   void finalize(const RedVals&) const;         thread 0 of the last block
+//   void finalize(const RedVals&) const;         one thread, after the fold
 #pragma once
+
+#include <type_traits>
 
 #include "aqp_common.cuh"
 
 namespace aqp {
 
+struct NoRowIn {};
+template <class Op, class = void>
+struct RowInOf {
+  using type = NoRowIn;
+  static constexpr bool value = false;
+};
 template <class Op>
-__global__ void __launch_bounds__(kThreads) spmv_op(DevCsr M, Op op, GridRed g) {
+struct RowInOf<Op, std::void_t<typename Op::RowIn>> {
+  using type = typename Op::RowIn;
+  static constexpr bool value = true;
+};
+
+template <class Op, class = void>
+struct SplitOf {
+  static constexpr bool value = false;
+};
+template <class Op>
+struct SplitOf<Op, std::void_t<decltype(Op::SPLIT)>> {
+  static constexpr bool value = Op::SPLIT;
+};
+
+// Fold per-block partials stored [slot][block] in block order (thread t takes
+// blocks t, t+256, ... with loads batched four blocks at a time), then the
+// fixed tree.  Result in thread 0.
+template <int NS, int NM>
+__device__ __forceinline__ void fold_partials(RedVals<NS, NM> &a, const double *partials, unsigned nb,
+                                              double *smem) {
+  constexpr int NT = NS + NM;
+  a.zero();
+  if constexpr (NT > 0) {
+    constexpr int U = 4;
+    for (unsigned b0 = threadIdx.x; b0 < nb; b0 += U * kThreads) {
+      double t[U][NT];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned b = b0 + u * kThreads;
+#pragma unroll
+        for (int i = 0; i < NT; ++i) t[u][i] = b < nb ? __ldcg(partials + (size_t)i * nb + b) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int i = 0; i < NS; ++i) a.s[i] += t[u][i];
+#pragma unroll
+        for (int i = 0; i < NM; ++i) a.m[i] = nanmax(a.m[i], t[u][NS + i]);
+      }
+    }
+  }
+  block_reduce<NS, NM>(a, smem);
+}
+
+// End of a reducing launch.  SPLIT: publish this block's partials and return
+// false.  Otherwise the last-block ticket: returns true in thread 0 of the
+// last block with the grid totals in `v`.
+template <int NS, int NM, bool SPLIT>
+__device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *smem) {
+  constexpr int NT = NS + NM;
+  __shared__ bool last;
+  if constexpr (NT > 0) block_reduce<NS, NM>(v, smem);
+  if (threadIdx.x == 0) {
+    const unsigned nb = gridDim.x;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) g.partials[(size_t)i * nb + blockIdx.x] = v.s[i];
+#pragma unroll
+    for (int i = 0; i < NM; ++i) g.partials[(size_t)(NS + i) * nb + blockIdx.x] = v.m[i];
+    if (!SPLIT) {
+      // only thread 0 published, so only thread 0 fences
+      __threadfence();
+      last = (atomicAdd(g.ticket, 1u) == nb - 1);
+      if (last) __threadfence();
+    }
+  }
+  if (SPLIT) return false;
+  __syncthreads();
+  if (!last) return false;
+  RedVals<NS, NM> a;
+  fold_partials<NS, NM>(a, g.partials, gridDim.x, smem);
+  v = a;
+  if (threadIdx.x == 0) *g.ticket = 0u;
+  return threadIdx.x == 0;
+}
+
+template <class Op>
+#ifndef AQP_SPMV_MIN_BLOCKS
+#define AQP_SPMV_MIN_BLOCKS 5
+#endif
+__global__ void __launch_bounds__(kThreads, AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
   constexpr int NS = Op::NS, NM = Op::NM;
   if (op.skip()) return;
   Op o = op;
   o.prepare();
-  __shared__ double sprod[kTileNnz];
-  __shared__ int scol[Op::SYM ? kTileNnz : 1];
+  // WARP-item staging buffer: dynamic, launched with M.smem_bytes (0 when the
+  // matrix has no WARP items, so THREAD-only passes keep full occupancy)
+  extern __shared__ double dyn_smem[];
+  double *sprod = dyn_smem;
+  int *scol = reinterpret_cast<int *>(dyn_smem + kTileNnz);
   __shared__ double sred[kWarps * kMaxRed];
-  const PlanItem it = M.plan[blockIdx.x];
   RedVals<NS, NM> acc;
   acc.zero();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (it.kind == kItemThread || it.kind == kItemWarp) {
+  PlanItem it;
+  if (M.uniform) {
+    it.kind = kItemThread;
+    it.row0 = blockIdx.x * kThreads;
+    it.row1 = min(it.row0 + kThreads, M.rows);
+  } else {
+    it = M.plan[blockIdx.x];
+  }
+
+  if (it.kind == kItemThread) {
+    // one thread per row, straight from HBM (no staging, no barrier)
+    const int r = it.row0 + threadIdx.x;
+    if (r < it.row1) {
+      using RowIn = typename RowInOf<Op>::type;
+      RowIn rin{};
+      if constexpr (RowInOf<Op>::value) rin = o.load_row(r);
+      const int b = __ldg(M.ptr + r), e = __ldg(M.ptr + r + 1);
+      double lo = 0.0, up = 0.0;
+      for (int k = b; k < e; ++k) {
+        const int c = __ldg(M.idx + k);
+        const double p = __ldg(M.val + k) * o.gather(c);
+        if (Op::SYM && c < r) lo += p; else up += p;
+      }
+      const double val = Op::SYM ? lo + up : up;
+      if constexpr (RowInOf<Op>::value) o.row_in(r, val, rin, acc); else o.row(r, val, acc);
+    }
+  } else if (it.kind == kItemWarp) {
+    // rows of medium length: stage the tile's products with coalesced loads,
+    // then one warp per row (tree order, deterministic)
     const int k0 = it.k0, k1 = it.k1;
-#pragma unroll 4
-    for (int k = k0 + threadIdx.x; k < k1; k += kThreads) {
-      const int c = __ldg(M.idx + k);
-      sprod[k - k0] = __ldg(M.val + k) * o.gather(c);
-      if constexpr (Op::SYM) scol[k - k0] = c;
+    int cs[kTileNnz / kThreads];
+#pragma unroll
+    for (int u = 0; u < kTileNnz / kThreads; ++u) {
+      const int k = k0 + threadIdx.x + u * kThreads;
+      cs[u] = k < k1 ? __ldg(M.idx + k) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kTileNnz / kThreads; ++u) {
+      const int k = k0 + threadIdx.x + u * kThreads;
+      if (k < k1) {
+        sprod[k - k0] = __ldg(M.val + k) * o.gather(cs[u]);
+        if constexpr (Op::SYM) scol[k - k0] = cs[u];
+      }
     }
     __syncthreads();
-    if (it.kind == kItemThread) {
-      const int r = it.row0 + threadIdx.x;
-      if (r < it.row1) {
-        const int b = __ldg(M.ptr + r) - k0, e = __ldg(M.ptr + r + 1) - k0;
-        double val;
-        if constexpr (Op::SYM) {
-          double lo = 0.0, up = 0.0;
-          for (int j = b; j < e; ++j) {
-            if (scol[j] < r) lo += sprod[j]; else up += sprod[j];
-          }
-          val = lo + up;
-        } else {
-          double a = 0.0;
-          for (int j = b; j < e; ++j) a += sprod[j];
-          val = a;
-        }
-        o.row(r, val, acc);
+    for (int r = it.row0 + warp; r < it.row1; r += kWarps) {
+      const int b = __ldg(M.ptr + r) - k0, e = __ldg(M.ptr + r + 1) - k0;
+      double lo = 0.0, up = 0.0;
+      for (int j = b + lane; j < e; j += 32) {
+        if (Op::SYM && scol[j] < r) lo += sprod[j]; else up += sprod[j];
       }
-    } else {
-      for (int r = it.row0 + warp; r < it.row1; r += kWarps) {
-        const int b = __ldg(M.ptr + r) - k0, e = __ldg(M.ptr + r + 1) - k0;
-        double lo = 0.0, up = 0.0;
-        for (int j = b + lane; j < e; j += 32) {
-          if (Op::SYM && scol[j] < r) lo += sprod[j]; else up += sprod[j];
-        }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          up += __shfl_xor_sync(0xffffffffu, up, off);
-          if constexpr (Op::SYM) lo += __shfl_xor_sync(0xffffffffu, lo, off);
-        }
-        if (lane == 0) o.row(r, Op::SYM ? lo + up : up, acc);
+      for (int off = 16; off > 0; off >>= 1) {
+        up += __shfl_xor_sync(0xffffffffu, up, off);
+        if constexpr (Op::SYM) lo += __shfl_xor_sync(0xffffffffu, lo, off);
       }
+      if (lane == 0) o.row(r, Op::SYM ? lo + up : up, acc);
     }
   } else if (it.kind == kItemLongSeq) {
     if (threadIdx.x == 0) {
@@ -94,6 +220,8 @@ __global__ void __launch_bounds__(kThreads) spmv_op(DevCsr M, Op op, GridRed g) 
       o.row(r, Op::SYM ? lo + up : up, acc);
     }
   } else {
+    // one segment of a long row: strided per-thread sums, fixed tree, then
+    // (if split) the last segment block folds the segment partials in order
     const int r = it.row0;
     RedVals<2, 0> lu;
     lu.zero();
@@ -112,10 +240,10 @@ __global__ void __launch_bounds__(kThreads) spmv_op(DevCsr M, Op op, GridRed g) 
         M.seg_part[2 * (it.segbase + it.seg) + 1] = lu.s[1];
         __threadfence();
         lastseg = (atomicAdd(M.seg_ticket + it.segbase, 1u) == (unsigned)(it.nseg - 1));
+        if (lastseg) __threadfence();
       }
       __syncthreads();
       if (lastseg && threadIdx.x == 0) {
-        __threadfence();
         double lo = 0.0, up = 0.0;
         for (int s = 0; s < it.nseg; ++s) {
           lo += __ldcg(M.seg_part + 2 * (it.segbase + s));
@@ -127,7 +255,7 @@ __global__ void __launch_bounds__(kThreads) spmv_op(DevCsr M, Op op, GridRed g) 
     }
   }
   if constexpr (Op::FINAL) {
-    if (grid_reduce<NS, NM>(acc, g, sred)) o.finalize(acc);
+    if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred)) o.finalize(acc);
   }
 }
 
@@ -141,12 +269,25 @@ __global__ void __launch_bounds__(kThreads) elem_op(int64_t n, Op op, GridRed g)
   RedVals<NS, NM> acc;
   acc.zero();
   const int64_t stride = (int64_t)gridDim.x * kThreads;
+#pragma unroll 4
   for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) o.elem(i, acc);
   if constexpr (Op::FINAL) {
-    if (grid_reduce<NS, NM>(acc, g, sred)) o.finalize(acc);
+    if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred)) o.finalize(acc);
   }
 }
 
+// the fold + finalize of a SPLIT op whose main launch had `nb` blocks
+template <class Op>
+__global__ void __launch_bounds__(kThreads) fin_op(Op op, GridRed g, unsigned nb) {
+  constexpr int NS = Op::NS, NM = Op::NM;
+  if (op.skip()) return;
+  Op o = op;
+  o.prepare();
+  __shared__ double sred[kWarps * kMaxRed];
+  RedVals<NS, NM> a;
+  fold_partials<NS, NM>(a, g.partials, nb, sred);
+  if (threadIdx.x == 0) o.finalize(a);
+}
 
 // grid of an elementwise pass: a pure function of n (so reductions are
 // reproducible), at most 8 resident 256-thread blocks on each of 148 SMs

@@ -81,11 +81,26 @@ static std::vector<PlanItem> plan_rows(const P *ptr, int64_t rows, bool strict, 
       ++i;
       continue;
     }
+    // THREAD item: up to 256 consecutive rows of <= kThreadRowMax nonzeros,
+    // one thread per row, sequential in column order (no shared memory)
+    const int64_t row_max = strict ? (int64_t)kTileNnz : (int64_t)kThreadRowMax;
     const int64_t start = i;
+    while (i < rows && i - start < kThreads && (int64_t)(ptr[i + 1] - ptr[i]) <= row_max) ++i;
+    if (i > start) {
+      PlanItem it{};
+      it.row0 = (int)start;
+      it.row1 = (int)i;
+      it.k0 = (int)ptr[start];
+      it.k1 = (int)ptr[i];
+      it.kind = kItemThread;
+      items.push_back(it);
+      continue;
+    }
+    // WARP item: medium rows staged in shared memory (<= kTileNnz per tile)
     int64_t nnz = 0;
     while (i < rows && i - start < kThreads) {
       const int64_t l = (int64_t)(ptr[i + 1] - ptr[i]);
-      if (l > kTileNnz || nnz + l > kTileNnz) break;
+      if (l <= row_max || l > kTileNnz || nnz + l > kTileNnz) break;
       nnz += l;
       ++i;
     }
@@ -94,9 +109,7 @@ static std::vector<PlanItem> plan_rows(const P *ptr, int64_t rows, bool strict, 
     it.row1 = (int)i;
     it.k0 = (int)ptr[start];
     it.k1 = (int)ptr[i];
-    // rows averaging more than ~24 nonzeros: a sequential per-thread chain
-    // would dominate; switch to one warp per row (tree order, deterministic)
-    it.kind = (!strict && nnz > 24 * (i - start)) ? kItemWarp : kItemThread;
+    it.kind = kItemWarp;
     items.push_back(it);
   }
   if (items.empty()) {  // zero rows: one empty item so fused finalizers still run
@@ -109,7 +122,9 @@ static std::vector<PlanItem> plan_rows(const P *ptr, int64_t rows, bool strict, 
 }
 
 int64_t plan_capacity(int64_t rows, int64_t nnz) {
-  return rows / 128 + 3 * (nnz / kTileNnz) + nnz / kSegNnz + 8;
+  // THREAD/WARP items break only at 256 rows, at a row-length class change
+  // or a full tile; long rows add their segments
+  return 2 * (rows / kThreads) + 2 * (nnz / kThreadRowMax) + 3 * (nnz / kTileNnz) + nnz / kSegNnz + 16;
 }
 
 // ---------------------------------------------------------------- setup kernels
@@ -235,6 +250,15 @@ int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *h
   AQP_CUDA(cudaStreamSynchronize(ctx->stream));  // `items` is pageable and local
   M.plan = plan_dev;
   M.nitems = (int)items.size();
+  bool warp_items = false;
+  for (const PlanItem &it : items) warp_items |= it.kind == kItemWarp;
+  M.smem_bytes = warp_items ? kTileNnz * (int)(sizeof(double) + sizeof(int)) : 0;
+  // uniform plans let the kernel derive its rows from blockIdx (no plan load)
+  bool uniform = M.rows > 0;
+  for (size_t b = 0; b < items.size() && uniform; ++b)
+    uniform = items[b].kind == kItemThread && items[b].row0 == (int)(b * kThreads) &&
+              items[b].row1 == (int)std::min<int64_t>((int64_t)(b + 1) * kThreads, M.rows);
+  M.uniform = uniform ? 1 : 0;
   M.nlongseg = nlong;
   M.seg_part = seg_part;
   M.seg_ticket = seg_ticket;

@@ -180,10 +180,10 @@ int run_csr_host(int kind, const int64_t *indptr, const int64_t *indices, const 
   }
   if (kind == 2) {
     OpRegStore<true> op{(const double *)dx.p, (double *)dout.p};
-    spmv_op<OpRegStore<true>><<<M->nitems, kThreads, 0, st>>>(*M, op, gr);
+    spmv_op<OpRegStore<true>><<<M->nitems, kThreads, M->smem_bytes, st>>>(*M, op, gr);
   } else {
     OpRegStore<false> op{(const double *)dx.p, (double *)dout.p};
-    spmv_op<OpRegStore<false>><<<M->nitems, kThreads, 0, st>>>(*M, op, gr);
+    spmv_op<OpRegStore<false>><<<M->nitems, kThreads, M->smem_bytes, st>>>(*M, op, gr);
   }
   AQP_CUDA(cudaGetLastError());
   int bad = 0;
