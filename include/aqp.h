@@ -230,7 +230,8 @@ int aqp_solver_reset_window(aqp_solver *s);   /* zero window sums, forget avg_pr
  * 3/4 = y-ray candidate 0/1, 5/6 = x-ray candidate 0/1 */
 int aqp_solver_read(aqp_solver *s, int which, double *host_out, int64_t len);
 /* launches_out[0]: kernels per outer iteration outside the BB loop;
- * launches_out[1]: kernels per BB iteration */
+ * launches_out[1]: kernels per BB iteration; launches_out[2]: 1 when the
+ * window graph uses programmatic (PDL) edges */
 int aqp_solver_counters(aqp_solver *s, int64_t *launches_out);
 /* Power iteration for the step size (linalg.py:287-312) on the solver's
  * buffers (call before aqp_solver_init).  *annihilated = 1 when A maps the
@@ -242,6 +243,11 @@ int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, do
  * launches follows an L2 flush (streaming read of flush_bytes at flush).  Average
  * device milliseconds per launch in *avg_ms.  Clobbers BB scratch. */
 int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, size_t flush_bytes, double *avg_ms);
+/* Device trace, enabled by AQP_TRACE=1 at solver creation: block 0 of every
+ * kernel stamps (tag = kind << 32 | grid size, %globaltimer ns); kind 0 SpMV
+ * pass, 1 vector pass, 2/3 fold-kernel start/end.  Copies up to `cap` pairs
+ * (2*cap words) and resets the ring. */
+int aqp_solver_trace(aqp_solver *s, unsigned long long *host_out, int64_t cap, int64_t *count);
 
 #ifdef __cplusplus
 }

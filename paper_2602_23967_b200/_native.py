@@ -119,6 +119,7 @@ SIGNATURES = {
     "aqp_solver_counters": (C.c_int, [_P, c_int64_p]),
     "aqp_solver_estimate_norm": (C.c_int, [_P, _P, C.c_int, c_double_p, C.POINTER(C.c_int)]),
     "aqp_solver_time_kernel": (C.c_int, [_P, C.c_int, C.c_int, _P, C.c_size_t, c_double_p]),
+    "aqp_solver_trace": (C.c_int, [_P, _P, _I64, c_int64_p]),
 }
 
 _lib = None

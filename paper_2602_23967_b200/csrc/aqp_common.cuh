@@ -115,7 +115,7 @@ struct RedVals {
 // thread 0.  Fixed xor-shuffle tree inside warps, then warp 0 folds the
 // per-warp values in warp order.
 template <int NS, int NM>
-__device__ __forceinline__ void block_reduce(RedVals<NS, NM> &v, double *smem /* kWarps*(NS+NM) */) {
+__device__ __forceinline__ void block_reduce(RedVals<NS, NM> &v, double *smem /* (blockDim/32)*(NS+NM) */) {
   constexpr int NT = NS + NM;
   if constexpr (NT == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -134,16 +134,17 @@ __device__ __forceinline__ void block_reduce(RedVals<NS, NM> &v, double *smem /*
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    const int nw = (int)(blockDim.x >> 5);
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
       double a = smem[i];
-      for (int w = 1; w < kWarps; ++w) a += smem[w * NT + i];
+      for (int w = 1; w < nw; ++w) a += smem[w * NT + i];
       v.s[i] = a;
     }
 #pragma unroll
     for (int i = 0; i < NM; ++i) {
       double a = smem[NS + i];
-      for (int w = 1; w < kWarps; ++w) a = nanmax(a, smem[w * NT + NS + i]);
+      for (int w = 1; w < nw; ++w) a = nanmax(a, smem[w * NT + NS + i]);
       v.m[i] = a;
     }
   }
@@ -154,7 +155,25 @@ __device__ __forceinline__ void block_reduce(RedVals<NS, NM> &v, double *smem /*
 struct GridRed {
   double *partials;     // >= kMaxRed * gridDim.x doubles, layout [slot][block]
   unsigned int *ticket;  // zero between launches (reset by the last block)
+  // optional device trace (AQP_TRACE=1): (tag, globaltimer ns) pairs
+  unsigned long long *trace = nullptr;
+  unsigned int *trace_n = nullptr;
+  unsigned int trace_cap = 0;
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// tag = kind << 32 | grid size (kind 0 spmv, 1 elem, 2 fin start, 3 fin end)
+__device__ __forceinline__ void trace_mark(const GridRed &g, unsigned kind) {
+  if (g.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned i = atomicAdd(g.trace_n, 1u) % g.trace_cap;
+    g.trace[2 * i] = ((unsigned long long)kind << 32) | gridDim.x;
+    g.trace[2 * i + 1] = global_ns();
+  }
+}
 
 // ---------------------------------------------------------------- SpMV work partition
 // One block per item.  THREAD: rows [row0,row1) whose nonzeros [k0,k1) fit

@@ -50,6 +50,15 @@
 
 namespace aqp {
 
+// Programmatic dependent launch (PDL).  Graph edges between consecutive
+// kernel nodes are programmatic: a kernel may be scheduled while its
+// predecessor drains; it reads nothing the predecessor produces before
+// pdl_wait() (griddepcontrol.wait: full completion + memory flush of the
+// predecessor), and releases its own dependents with pdl_trigger() once its
+// main work is issued.  Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct NoRowIn {};
 template <class Op, class = void>
 struct RowInOf {
@@ -81,13 +90,14 @@ __device__ __forceinline__ void fold_partials(RedVals<NS, NM> &a, const double *
   a.zero();
   if constexpr (NT > 0) {
     constexpr int U = 4;
-    for (unsigned b0 = threadIdx.x; b0 < nb; b0 += U * kThreads) {
+    const unsigned nt = blockDim.x;
+    for (unsigned b0 = threadIdx.x; b0 < nb; b0 += U * nt) {
       double t[U][NT];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const unsigned b = b0 + u * kThreads;
+        const unsigned b = b0 + u * nt;
 #pragma unroll
-        for (int i = 0; i < NT; ++i) t[u][i] = b < nb ? __ldcg(partials + (size_t)i * nb + b) : 0.0;
+        for (int i = 0; i < NT; ++i) t[u][i] = b < nb ? partials[(size_t)i * nb + b] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -132,12 +142,26 @@ __device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *
   return threadIdx.x == 0;
 }
 
-template <class Op>
 #ifndef AQP_SPMV_MIN_BLOCKS
-#define AQP_SPMV_MIN_BLOCKS 5
+#define AQP_SPMV_MIN_BLOCKS 4
 #endif
-__global__ void __launch_bounds__(kThreads, AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
+// UNIFORM: the plan is all THREAD items over [256 b, 256 b + 256) (the common
+// case of short-row matrices, e.g. every C2 pass); the instantiation then
+// carries only the thread-per-row path, which needs far fewer registers
+template <class Op, bool UNIFORM = false>
+__global__ void __launch_bounds__(kThreads, UNIFORM ? 5 : AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
   constexpr int NS = Op::NS, NM = Op::NM;
+  // static matrix data first: the plan item does not depend on the predecessor
+  PlanItem it;
+  if (UNIFORM || M.uniform) {
+    it.kind = kItemThread;
+    it.row0 = blockIdx.x * kThreads;
+    it.row1 = min(it.row0 + kThreads, M.rows);
+  } else {
+    it = M.plan[blockIdx.x];
+  }
+  pdl_wait();
+  trace_mark(g, 0);
   if (op.skip()) return;
   Op o = op;
   o.prepare();
@@ -150,14 +174,6 @@ __global__ void __launch_bounds__(kThreads, AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr 
   RedVals<NS, NM> acc;
   acc.zero();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  PlanItem it;
-  if (M.uniform) {
-    it.kind = kItemThread;
-    it.row0 = blockIdx.x * kThreads;
-    it.row1 = min(it.row0 + kThreads, M.rows);
-  } else {
-    it = M.plan[blockIdx.x];
-  }
 
   if (it.kind == kItemThread) {
     // one thread per row, straight from HBM (no staging, no barrier)
@@ -176,6 +192,8 @@ __global__ void __launch_bounds__(kThreads, AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr 
       const double val = Op::SYM ? lo + up : up;
       if constexpr (RowInOf<Op>::value) o.row_in(r, val, rin, acc); else o.row(r, val, acc);
     }
+  } else if (UNIFORM) {
+    // not reached: uniform plans hold THREAD items only
   } else if (it.kind == kItemWarp) {
     // rows of medium length: stage the tile's products with coalesced loads,
     // then one warp per row (tree order, deterministic)
@@ -254,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr 
       }
     }
   }
+  pdl_trigger();
   if constexpr (Op::FINAL) {
     if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred)) o.finalize(acc);
   }
@@ -262,6 +281,8 @@ __global__ void __launch_bounds__(kThreads, AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr 
 template <class Op>
 __global__ void __launch_bounds__(kThreads) elem_op(int64_t n, Op op, GridRed g) {
   constexpr int NS = Op::NS, NM = Op::NM;
+  pdl_wait();
+  trace_mark(g, 1);
   if (op.skip()) return;
   Op o = op;
   o.prepare();
@@ -271,6 +292,7 @@ __global__ void __launch_bounds__(kThreads) elem_op(int64_t n, Op op, GridRed g)
   const int64_t stride = (int64_t)gridDim.x * kThreads;
 #pragma unroll 4
   for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) o.elem(i, acc);
+  pdl_trigger();
   if constexpr (Op::FINAL) {
     if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred)) o.finalize(acc);
   }
@@ -280,6 +302,9 @@ __global__ void __launch_bounds__(kThreads) elem_op(int64_t n, Op op, GridRed g)
 template <class Op>
 __global__ void __launch_bounds__(kThreads) fin_op(Op op, GridRed g, unsigned nb) {
   constexpr int NS = Op::NS, NM = Op::NM;
+  pdl_wait();
+  pdl_trigger();  // one block: let the next kernel's blocks get resident now
+  trace_mark(g, 2);
   if (op.skip()) return;
   Op o = op;
   o.prepare();
@@ -287,6 +312,7 @@ __global__ void __launch_bounds__(kThreads) fin_op(Op op, GridRed g, unsigned nb
   RedVals<NS, NM> a;
   fold_partials<NS, NM>(a, g.partials, nb, sred);
   if (threadIdx.x == 0) o.finalize(a);
+  trace_mark(g, 3);
 }
 
 // grid of an elementwise pass: a pure function of n (so reductions are

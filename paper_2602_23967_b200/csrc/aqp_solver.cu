@@ -17,7 +17,9 @@
 //
 // All scalars (alpha, best phi, tolerances, counters, slot indices) live in a
 // device control block; the host only reads it at certification points.
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstddef>
 #include <cstdlib>
 #include <cstring>
@@ -28,6 +30,8 @@
 #include "aqp_kernels.cuh"
 
 namespace aqp {
+
+constexpr int kFinThreads = 1024;  // fold block: 4x the loads in flight of a 256-thread block
 
 // ---------------------------------------------------------------- control block
 enum RedSlot : int {
@@ -861,6 +865,40 @@ __global__ void k_pw_check(Ctrl *ct, int slot) {
   if (ct->red[slot] == 0.0) ct->pw_stop = 1;  // linalg.py:309 `if nw == 0.0: break`
 }
 
+// Fold + finalize for the solver's SPLIT ops.  The finalize code (BB step
+// rule, tolerance update, slot rotation) is a chain of dependent reads and
+// writes of the control block; run on global memory that chain cost ~19 us
+// per BB iteration (device trace).  Here the block stages the whole control
+// block in shared memory with one coalesced copy (overlapping the fold),
+// thread 0 finalizes against the staged copy, and the block writes it back.
+template <class Op>
+__global__ void __launch_bounds__(kFinThreads) fin_ctrl_op(Op op, GridRed g, unsigned nb) {
+  constexpr int NS = Op::NS, NM = Op::NM;
+  static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl must be a whole number of words");
+  constexpr int W = (int)(sizeof(Ctrl) / 8);
+  __shared__ unsigned long long cbuf[W];
+  __shared__ double sred[(kFinThreads / 32) * kMaxRed];
+  pdl_wait();
+  pdl_trigger();
+  trace_mark(g, 2);
+  if (op.skip()) return;
+  Ctrl *gctrl = op.v.ctrl;
+  const unsigned long long *src = reinterpret_cast<const unsigned long long *>(gctrl);
+  for (int i = threadIdx.x; i < W; i += blockDim.x) cbuf[i] = __ldcg(src + i);
+  RedVals<NS, NM> a;
+  fold_partials<NS, NM>(a, g.partials, nb, sred);  // ends with __syncthreads
+  trace_mark(g, 4);
+  Op o = op;
+  o.v.ctrl = reinterpret_cast<Ctrl *>(cbuf);
+  o.prepare();
+  if (threadIdx.x == 0) o.finalize(a);
+  trace_mark(g, 5);
+  __syncthreads();
+  unsigned long long *dst = reinterpret_cast<unsigned long long *>(gctrl);
+  for (int i = threadIdx.x; i < W; i += blockDim.x) dst[i] = cbuf[i];
+  trace_mark(g, 3);
+}
+
 }  // namespace aqp
 
 using namespace aqp;
@@ -878,6 +916,7 @@ struct aqp_solver {
   int64_t launches_per_iter_fixed = 0;
   int64_t kernel_launches = 0;
   bool eager = false;
+  bool pdl = false;
 };
 
 namespace {
@@ -909,52 +948,85 @@ void layout_solver(Bump &b, aqp_problem *p, SV &v, Ctrl **ctrl, GridRed &gr) {
 }
 
 // explicit graph construction helpers
+static bool g_use_pdl = true;
+// a graph cursor: the last node added and whether it is a kernel node
+// (cudaGraphNodeGetType fails on conditional nodes with this runtime)
+struct GNode {
+  cudaGraphNode_t n = nullptr;
+  bool kernel = false;
+};
+
 template <class K, class... A>
-cudaError_t add_node_smem(cudaGraph_t g, cudaGraphNode_t &last, unsigned grid, unsigned smem, K fn, A... args) {
+cudaError_t add_node_cfg(cudaGraph_t g, GNode &last, unsigned grid, unsigned block, unsigned smem, K fn,
+                         A... args) {
   void *params[] = {(void *)&args...};
   cudaKernelNodeParams kp = {};
   kp.func = (void *)fn;
   kp.gridDim = dim3(grid);
-  kp.blockDim = dim3(kThreads);
+  kp.blockDim = dim3(block);
   kp.sharedMemBytes = smem;
   kp.kernelParams = params;
   kp.extra = nullptr;
   cudaGraphNode_t node;
-  cudaError_t e = cudaGraphAddKernelNode(&node, g, last ? &last : nullptr, last ? 1 : 0, &kp);
-  if (e == cudaSuccess) last = node;
+  cudaError_t e;
+  if (last.n && last.kernel && g_use_pdl) {
+    // kernel -> kernel edge: programmatic (PDL)
+    e = cudaGraphAddKernelNode(&node, g, nullptr, 0, &kp);
+    if (e != cudaSuccess) return e;
+    cudaGraphEdgeData ed = {};
+    ed.from_port = cudaGraphKernelNodePortProgrammatic;
+    ed.type = cudaGraphDependencyTypeProgrammatic;
+    e = cudaGraphAddDependencies_v2(g, &last.n, &node, &ed, 1);
+  } else {
+    e = cudaGraphAddKernelNode(&node, g, last.n ? &last.n : nullptr, last.n ? 1 : 0, &kp);
+  }
+  if (e == cudaSuccess) {
+    last.n = node;
+    last.kernel = true;
+  }
   return e;
 }
 template <class K, class... A>
-cudaError_t add_node(cudaGraph_t g, cudaGraphNode_t &last, unsigned grid, K fn, A... args) {
+cudaError_t add_node_smem(cudaGraph_t g, GNode &last, unsigned grid, unsigned smem, K fn, A... args) {
+  return add_node_cfg(g, last, grid, (unsigned)kThreads, smem, fn, args...);
+}
+template <class K, class... A>
+cudaError_t add_node(cudaGraph_t g, GNode &last, unsigned grid, K fn, A... args) {
   return add_node_smem(g, last, grid, 0u, fn, args...);
 }
 
 template <class Op>
-cudaError_t node_spmv(cudaGraph_t g, cudaGraphNode_t &last, const DevCsr &M, const Op &op, GridRed gr) {
+cudaError_t node_spmv(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
+  if (M.uniform) return add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_op<Op, true>, M, op, gr);
   return add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M, op, gr);
 }
 template <class Op>
-cudaError_t node_elem(cudaGraph_t g, cudaGraphNode_t &last, int64_t n, const Op &op, GridRed gr) {
+cudaError_t node_elem(cudaGraph_t g, GNode &last, int64_t n, const Op &op, GridRed gr) {
   return add_node(g, last, (unsigned)elem_grid(n), elem_op<Op>, n, op, gr);
 }
 
 // SPLIT ops: the main launch followed by its one-block fold/finalize
 template <class Op>
-cudaError_t node_spmv_fin(cudaGraph_t g, cudaGraphNode_t &last, const DevCsr &M, const Op &op, GridRed gr) {
-  cudaError_t e = add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M, op, gr);
+cudaError_t node_spmv_fin(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
+  cudaError_t e = M.uniform ? add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_op<Op, true>, M, op, gr)
+                            : add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M,
+                                            op, gr);
   if (e != cudaSuccess) return e;
-  return add_node(g, last, 1u, fin_op<Op>, op, gr, (unsigned)M.nitems);
+  return add_node_cfg(g, last, 1u, (unsigned)kFinThreads, 0u, fin_ctrl_op<Op>, op, gr, (unsigned)M.nitems);
 }
 template <class Op>
-cudaError_t node_elem_fin(cudaGraph_t g, cudaGraphNode_t &last, int64_t n, const Op &op, GridRed gr) {
+cudaError_t node_elem_fin(cudaGraph_t g, GNode &last, int64_t n, const Op &op, GridRed gr) {
   cudaError_t e = add_node(g, last, (unsigned)elem_grid(n), elem_op<Op>, n, op, gr);
   if (e != cudaSuccess) return e;
-  return add_node(g, last, 1u, fin_op<Op>, op, gr, (unsigned)elem_grid(n));
+  return add_node_cfg(g, last, 1u, (unsigned)kFinThreads, 0u, fin_ctrl_op<Op>, op, gr, (unsigned)elem_grid(n));
 }
 
 template <class Op>
 cudaError_t run_spmv(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
-  spmv_op<Op><<<M.nitems, kThreads, M.smem_bytes, st>>>(M, op, gr);
+  if (M.uniform)
+    spmv_op<Op, true><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
+  else
+    spmv_op<Op><<<M.nitems, kThreads, M.smem_bytes, st>>>(M, op, gr);
   return cudaGetLastError();
 }
 template <class Op>
@@ -964,18 +1036,21 @@ cudaError_t run_elem(cudaStream_t st, int64_t n, const Op &op, GridRed gr) {
 }
 template <class Op>
 cudaError_t run_spmv_fin(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
-  spmv_op<Op><<<M.nitems, kThreads, M.smem_bytes, st>>>(M, op, gr);
-  fin_op<Op><<<1, kThreads, 0, st>>>(op, gr, (unsigned)M.nitems);
+  if (M.uniform)
+    spmv_op<Op, true><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
+  else
+    spmv_op<Op><<<M.nitems, kThreads, M.smem_bytes, st>>>(M, op, gr);
+  fin_ctrl_op<Op><<<1, kFinThreads, 0, st>>>(op, gr, (unsigned)M.nitems);
   return cudaGetLastError();
 }
 template <class Op>
 cudaError_t run_elem_fin(cudaStream_t st, int64_t n, const Op &op, GridRed gr) {
   elem_op<Op><<<elem_grid(n), kThreads, 0, st>>>(n, op, gr);
-  fin_op<Op><<<1, kThreads, 0, st>>>(op, gr, (unsigned)elem_grid(n));
+  fin_ctrl_op<Op><<<1, kFinThreads, 0, st>>>(op, gr, (unsigned)elem_grid(n));
   return cudaGetLastError();
 }
 
-int add_lowrank(aqp_solver *s, cudaGraph_t g, cudaGraphNode_t &last, int src) {
+int add_lowrank(aqp_solver *s, cudaGraph_t g, GNode &last, int src) {
   aqp_problem *p = s->p;
   OpRx rx{};
   rx.v = s->v;
@@ -1015,7 +1090,7 @@ int build_graph(aqp_solver *s) {
   SV v = s->v;
   v.in_graph = 1;
   GridRed gr = s->gr;
-  cudaGraphNode_t last = nullptr;
+  GNode last;
   int64_t fixed = 0;
   if (diag) {
     OpP1Diag o{};
@@ -1038,10 +1113,11 @@ int build_graph(aqp_solver *s) {
     ip.conditional.type = cudaGraphCondTypeWhile;
     ip.conditional.size = 1;
     cudaGraphNode_t inner;
-    AQP_CUDA(cudaGraphAddNode(&inner, body, &last, 1, &ip));
-    last = inner;
+    AQP_CUDA(cudaGraphAddNode(&inner, body, &last.n, 1, &ip));
+    last.n = inner;
+    last.kernel = false;
     cudaGraph_t ib = ip.conditional.phGraph_out[0];
-    cudaGraphNode_t il = nullptr;
+    GNode il;
     OpStep st{};
     st.v = v;
     AQP_CUDA(node_elem(ib, il, p->n, st, gr));
@@ -1061,6 +1137,24 @@ int build_graph(aqp_solver *s) {
   s->launches_per_iter_fixed = fixed;
   AQP_CUDA(cudaGraphInstantiate(&s->exec, g, 0));
   return AQP_OK;
+}
+
+int build_graph_any(aqp_solver *s) {
+  const char *env = getenv("AQP_NO_PDL");
+  g_use_pdl = !(env && env[0] == '1');
+  int rc = build_graph(s);
+  if (rc != AQP_OK && g_use_pdl) {
+    // programmatic edges rejected (e.g. inside conditional bodies): plain edges
+    const std::string first = aqp_last_error();
+    if (s->graph) cudaGraphDestroy(s->graph);
+    s->graph = nullptr;
+    cudaGetLastError();
+    g_use_pdl = false;
+    rc = build_graph(s);
+    if (rc != AQP_OK) set_error(first + " | without PDL: " + aqp_last_error());
+  }
+  s->pdl = g_use_pdl;
+  return rc;
 }
 
 // Push only the host-owned prefix of the control block (aqp_scalars + tau,
@@ -1157,9 +1251,17 @@ int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, si
   s->h.xcur = 0; s->h.xprev = 1; s->h.ycur = 0; s->h.yprev = 1;
   const char *eager = getenv("AQP_EAGER");
   s->eager = eager && eager[0] == '1';
+  const char *trace = getenv("AQP_TRACE");
+  if (trace && trace[0] == '1') {
+    // debug facility: a device ring of (tag, ns) stamps, outside the workspace
+    s->gr.trace_cap = 1u << 20;
+    AQP_CUDA(cudaMalloc(&s->gr.trace, sizeof(unsigned long long) * 2 * s->gr.trace_cap));
+    AQP_CUDA(cudaMalloc(&s->gr.trace_n, sizeof(unsigned)));
+    AQP_CUDA(cudaMemset(s->gr.trace_n, 0, sizeof(unsigned)));
+  }
   cudaStream_t st = p->ctx->stream;
   AQP_CUDA(cudaMemsetAsync(s->gr.ticket, 0, 64, st));
-  int rc = build_graph(s);
+  int rc = build_graph_any(s);
   if (rc) {
     delete s;
     return rc;
@@ -1170,6 +1272,8 @@ int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, si
 
 int aqp_solver_destroy(aqp_solver *s) {
   if (!s) return AQP_OK;
+  if (s->gr.trace) cudaFree(s->gr.trace);
+  if (s->gr.trace_n) cudaFree(s->gr.trace_n);
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->graph) cudaGraphDestroy(s->graph);
   delete s;
@@ -1395,6 +1499,7 @@ int aqp_solver_read(aqp_solver *s, int which, double *host_out, int64_t len) {
 int aqp_solver_counters(aqp_solver *s, int64_t *out) {
   if (!s || !out) return fail(AQP_EINVAL, "NULL argument");
   out[0] = s->launches_per_iter_fixed;
+  out[2] = s->pdl ? 1 : 0;
   out[1] = s->p->quad_kind == AQP_QUAD_DIAGONAL ? 0 : (s->p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK ? 5 : 3);
   return AQP_OK;
 }
@@ -1522,6 +1627,26 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   *avg_ms = total / reps;
+  return AQP_OK;
+}
+
+// Device trace (AQP_TRACE=1): copies up to `cap` (tag, ns) pairs, oldest
+// first, and resets the ring; *count = pairs copied (0 when tracing is off).
+int aqp_solver_trace(aqp_solver *s, unsigned long long *host_out, int64_t cap, int64_t *count) {
+  if (!s || !count) return fail(AQP_EINVAL, "NULL argument");
+  *count = 0;
+  if (!s->gr.trace) return AQP_OK;
+  cudaStream_t st = s->p->ctx->stream;
+  unsigned n = 0;
+  AQP_CUDA(cudaMemcpyAsync(&n, s->gr.trace_n, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  const int64_t m = std::min<int64_t>({(int64_t)n, (int64_t)s->gr.trace_cap, cap});
+  if (m > 0 && host_out) {
+    AQP_CUDA(cudaMemcpyAsync(host_out, s->gr.trace, sizeof(unsigned long long) * 2 * m, cudaMemcpyDeviceToHost, st));
+  }
+  AQP_CUDA(cudaMemsetAsync(s->gr.trace_n, 0, sizeof(unsigned), st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  *count = m;
   return AQP_OK;
 }
 

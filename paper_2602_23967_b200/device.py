@@ -210,10 +210,22 @@ class DeviceSolver:
                   "aqp_solver_time_kernel")
         return out.value
 
+    def trace(self, cap: int = 1 << 20) -> np.ndarray:
+        """(tag, ns) stamps recorded since the last call (AQP_TRACE=1), as an (k, 2) uint64 array."""
+        buf = np.empty(2 * cap, dtype=np.uint64)
+        cnt = C.c_int64()
+        nat.check(self.lib.aqp_solver_trace(self.handle, buf.ctypes.data, cap, C.byref(cnt)), "aqp_solver_trace")
+        return buf[: 2 * cnt.value].reshape(-1, 2)
+
     def counters(self):
-        buf = (C.c_int64 * 2)()
+        buf = (C.c_int64 * 3)()
         nat.check(self.lib.aqp_solver_counters(self.handle, buf))
         return int(buf[0]), int(buf[1])
+
+    def uses_pdl(self) -> bool:
+        buf = (C.c_int64 * 3)()
+        nat.check(self.lib.aqp_solver_counters(self.handle, buf))
+        return bool(buf[2])
 
     def close(self):
         if getattr(self, "handle", None):

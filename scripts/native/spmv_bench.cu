@@ -508,6 +508,57 @@ __global__ void __launch_bounds__(T) v11(int ntiles, const Tile *tiles, const in
   if (threadIdx.x == 0) { for (int i = 0; i < 7; ++i) out[i] = s[i]; *ticket = 0; }
 }
 
+// V12: v9 body (no ticket) but every pointer comes from a slot index read from
+// global memory first (the library's rotating BB buffers)
+struct Slots { int xt, xo, go, g; };
+__global__ void __launch_bounds__(T) v12(int n, const int *ptr, const int *idx, const double *val, const double *bufs,
+                                         const Slots *slots, Vecs v, double *part) {
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  __shared__ double sred[64];
+  const Slots sl = *slots;
+  const double *xt = bufs + (long)sl.xt * n, *xo = bufs + (long)sl.xo * n, *go = bufs + (long)sl.go * n;
+  double *gt = const_cast<double *>(bufs) + (long)sl.g * n;
+  const int r = blockIdx.x * T + threadIdx.x;
+  if (r < n) {
+    const double x = xt[r], c = v.cen[r], l = v.lin[r], lo = v.lo[r], hi = v.hi[r], xov = xo[r], gov = go[r];
+    const int b = __ldg(ptr + r), e = __ldg(ptr + r + 1);
+    double lo_s = 0.0, up_s = 0.0;
+    for (int k = b; k < e; ++k) {
+      const int col = __ldg(idx + k);
+      const double p = __ldg(val + k) * __ldg(xt + col);
+      if (col < r) lo_s += p; else up_s += p;
+    }
+    const double a = lo_s + up_s;
+    const double g = (a + l) + (x - c) / v.tau;
+    gt[r] = g;
+    const double nr = x - clip(x - g, lo, hi);
+    acc[0] += nr * nr; acc[1] += x * g; acc[2] += l * x; acc[3] += (x - c) * c;
+    const double sd = x - xov, vd = g - gov;
+    acc[4] += sd * vd; acc[5] += sd * sd; acc[6] += vd * vd;
+  }
+  block_sum<7>(acc, sred);
+  if (threadIdx.x == 0) for (int i = 0; i < 7; ++i) part[i * gridDim.x + blockIdx.x] = acc[i];
+}
+
+// fold probes: 7 x nb partials stored [slot][block]
+template <int TH, int MODE>
+__global__ void __launch_bounds__(TH) fold_probe(int nb, const double *part, double *out) {
+  double s[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < nb; b += TH)
+#pragma unroll
+    for (int i = 0; i < 7; ++i) s[i] += MODE ? __ldcg(part + (long)i * nb + b) : part[(long)i * nb + b];
+  __shared__ double sm[TH / 32][7];
+#pragma unroll
+  for (int off = 16; off; off >>= 1)
+#pragma unroll
+    for (int i = 0; i < 7; ++i) s[i] += __shfl_xor_sync(~0u, s[i], off);
+  if ((threadIdx.x & 31) == 0)
+    for (int i = 0; i < 7; ++i) sm[threadIdx.x >> 5][i] = s[i];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 7; ++i) { double a = 0; for (int w = 0; w < TH / 32; ++w) a += sm[w][i]; out[i] = a; }
+}
+
 // gather-only probes: sum_k val[k] * x[idx[k]] with different cache operators (MODE 0 ldg, 1 ldcg, 2 plain)
 template <int MODE>
 __global__ void gather_only(long nnz, const int *idx, const double *val, const double *x, double *sink) {
@@ -638,6 +689,20 @@ int main(int argc, char **argv) {
     timeit("v9 row/thr + ticket", [&] { v9<false, true><<<gb, T>>>(n, dptr, didx, dval, dd, v, part, tk, outv); });
     timeit("v9 row/thr no ticket", [&] { v9<false, false><<<gb, T>>>(n, dptr, didx, dval, dd, v, part, tk, outv); });
     timeit("v9 diag-split + ticket", [&] { v9<true, true><<<gb, T>>>(n, dp2, di2, dv2, dd, v, part, tk, outv); });
+    {
+      double *bufs; Slots *dsl; Slots hs{1, 2, 3, 4};
+      CK(cudaMalloc(&bufs, 5L * n * 8)); CK(cudaMemset(bufs, 0, 5L * n * 8)); CK(cudaMalloc(&dsl, sizeof(Slots)));
+      CK(cudaMemcpy(dsl, &hs, sizeof hs, cudaMemcpyHostToDevice));
+      timeit("v12 slot-indirect pointers", [&] { v12<<<gb, T>>>(n, dptr, didx, dval, bufs, dsl, v, part); });
+      timeit("v9 row/thr no ticket (again)", [&] { v9<false, false><<<gb, T>>>(n, dptr, didx, dval, dd, v, part, tk, outv); });
+    }
+    {
+      const int nbp = 3907;
+      timeit("fold 256 plain", [&] { fold_probe<256, 0><<<1, 256>>>(nbp, part, outv); });
+      timeit("fold 256 cg", [&] { fold_probe<256, 1><<<1, 256>>>(nbp, part, outv); });
+      timeit("fold 1024 plain", [&] { fold_probe<1024, 0><<<1, 1024>>>(nbp, part, outv); });
+      timeit("empty-ish 1 block", [&] { fold_probe<256, 0><<<1, 256>>>(1, part, outv); });
+    }
     for (int bps : {2, 4, 6, 8}) {
       char nm[64];
       snprintf(nm, sizeof nm, "v11 one-wave x%d/SM", bps);
