@@ -228,16 +228,17 @@ def run_ours(args, world, rank, local):
     for kid, name, nbytes in ((0, "bb_gradient", 12 * nnz_q + 4 * (n + 1) + 64 * n),
                               (1, "bb_step", 40 * n),
                               (2, "p1_At_y", 12 * dev.info.at_nnz + 4 * (n + 1) + 8 * m + 8 * n + 16 * n + 16 * n),
-                              (3, "p2_A_xbar", 12 * dev.info.a_nnz + 4 * (m + 1) + 8 * n + 48 * m)):
+                              (3, "p2_A_xbar", 12 * dev.info.a_nnz + 4 * (m + 1) + 8 * n + 48 * m),
+                              (5, "bb_fold", 8 * 7 * dev.info.q_items)):
         sol.time_kernel(kid, 3, flush)
         avg = sol.time_kernel(kid, 20, flush)
         kernels[name] = {"ms": avg, "alg_bytes": nbytes, "gbs": nbytes / (avg * 1e-3) / 1e9}
     top = kernels["bb_gradient"]
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("bb_gradient", {}).get("dram_bytes_per_launch")
+            traffic = json.load(open(prof))["kernels"]["bb_gradient"]["dram_bytes_per_launch"]
         except Exception:
             traffic = None
     fixed, per_inner = sol.counters()

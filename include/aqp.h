@@ -239,7 +239,8 @@ int aqp_solver_counters(aqp_solver *s, int64_t *launches_out);
 int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, double *out,
                              int *annihilated);
 /* Stand-alone event timing of one hot kernel (bench.py roofline): kernel
- * 0 = BB gradient pass, 1 = BB step, 2 = P1, 3 = P2, 4 = X; each of `reps`
+ * 0 = BB gradient SpMV pass, 1 = BB step, 2 = P1, 3 = P2 (+fold), 4 = X
+ * (+fold), 5 = fold/finalize of pass 0; each of `reps`
  * launches follows an L2 flush (streaming read of flush_bytes at flush).  Average
  * device milliseconds per launch in *avg_ms.  Clobbers BB scratch. */
 int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, size_t flush_bytes, double *avg_ms);

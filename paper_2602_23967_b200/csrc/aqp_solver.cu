@@ -1556,9 +1556,10 @@ __global__ void k_flush_read(const double2 *p, int64_t n2, double *sink) {
 // Stand-alone timing of one hot kernel (for the roofline in bench.py): `reps`
 // launches on the solver stream, each preceded by an L2 flush (a write of
 // `flush_bytes` to `flush`), timed with events around the kernel only.
-// kernel: 0 = BB gradient pass (Q SpMV + epilogue + 7 reductions),
+// kernel: 0 = BB gradient pass (Q SpMV + epilogue + 7 partial sums),
 //         1 = BB step (x_t = clamp(x - alpha g)), 2 = P1 (A'y + epilogue),
-//         3 = P2 (A xbar + dual epilogue), 4 = X (primal epilogue).
+//         3 = P2 (A xbar + dual epilogue + fold), 4 = X (primal epilogue +
+//         fold), 5 = the fold/finalize kernel of pass 0.
 // Run after aqp_solver_init; it overwrites BB scratch and the control block's
 // BB fields, so re-init before solving.
 int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, size_t flush_bytes, double *avg_ms) {
@@ -1586,10 +1587,17 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
     }
     AQP_CUDA(cudaEventRecord(e0, st));
     switch (kernel) {
-      case 0: {
+      case 0: {  // the SpMV pass alone (its partials fold is kernel 5)
         OpGrad<false> o{};
         o.v = v;
-        AQP_CUDA(run_spmv_fin(st, p->Q, o, gr));
+        AQP_CUDA(run_spmv(st, p->Q, o, gr));
+        break;
+      }
+      case 5: {
+        OpGrad<false> o{};
+        o.v = v;
+        fin_ctrl_op<OpGrad<false>><<<1, kFinThreads, 0, st>>>(o, gr, (unsigned)p->Q.nitems);
+        AQP_CUDA(cudaGetLastError());
         break;
       }
       case 1: {

@@ -18,7 +18,8 @@ nq = dev.info.q_full_nnz
 out = {}
 for kid, name, nbytes in ((0, "bb_gradient", 12 * nq + 4 * (n + 1) + 64 * n), (1, "bb_step", 40 * n),
                           (2, "p1", 12 * dev.info.at_nnz + 4 * (n + 1) + 8 * m + 24 * n),
-                          (3, "p2", 12 * dev.info.a_nnz + 4 * (m + 1) + 8 * n + 48 * m), (4, "xpost", 48 * n)):
+                          (3, "p2", 12 * dev.info.a_nnz + 4 * (m + 1) + 8 * n + 48 * m), (4, "xpost", 48 * n),
+                          (5, "bb_fold", 8 * 7 * dev.info.q_items)):
     sol.time_kernel(kid, 3, flush)
     ms = sol.time_kernel(kid, 30, flush)
     ms_warm = sol.time_kernel(kid, 30, None)

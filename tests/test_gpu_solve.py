@@ -46,6 +46,8 @@ GOLDENS = [
     ("c4u:1e3:1", "ref_c4u_1e3_1.json"), ("c4i:1e3:1", "ref_c4i_1e3_1.json"),
     ("c4ur:1e3:1", "ref_c4ur_1e3_1.json"), ("c4ir:1e3:1", "ref_c4ir_1e3_1.json"),
     ("c4ur:1e4:1", "ref_c4ur_1e4_1.json"), ("c4ir:1e4:1", "ref_c4ir_1e4_1.json"),
+    ("c4u:1e4:1", "ref_c4u_1e4_1.json"), ("c4i:1e4:1", "ref_c4i_1e4_1.json"),
+    ("c4u:1e5:1", "ref_c4u_1e5_1.json"), ("c4i:1e5:1", "ref_c4i_1e5_1.json"),
     ("c2:1e4:5e3:0", "ref_c2_1e4_5e3_0.json"),
     ("c3:2e3:100:0", "ref_c3_2e3_100_0.json"), ("c3:2e4:100:0", "ref_c3_2e4_100_0.json"),
     ("c5:5e4:500:0", "ref_c5_5e4_500_0.json"), ("c5:5e4:500:0:diag", "ref_c5_5e4_500_0_diag.json"),
