@@ -148,6 +148,19 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *desc,
                        void *persistent, size_t persistent_bytes,
                        void *scratch, size_t scratch_bytes, aqp_problem **out);
 int aqp_problem_get_info(const aqp_problem *p, aqp_problem_info *out);
+
+/* Row shard of a multi-GPU solve (the reference has no
+ * multi-GPU path -- its only parallelism is a process pool over instances,
+ * anchorqp/bench.py:89-98).  Rank `rank` of `nranks` (<= 8) owns rows
+ * [n0,n1) of A' and Q (x side) and rows [m0,m1) of A (y side); every rank
+ * creates the whole problem, then restricts its passes to its rows.  Not
+ * available for the low-rank Q kind. */
+typedef struct {
+  int32_t rank, nranks;
+  int64_t n0, n1;
+  int64_t m0, m1;
+} aqp_shard;
+int aqp_problem_shard(aqp_problem *p, const aqp_shard *sh);
 int aqp_problem_destroy(aqp_problem *p);
 
 
@@ -209,6 +222,16 @@ int aqp_solver_sizes(const aqp_problem *p, size_t *workspace_bytes);
 int aqp_solver_create(aqp_problem *p, const aqp_solver_params *params, void *workspace,
                       size_t workspace_bytes, aqp_solver **out);
 int aqp_solver_destroy(aqp_solver *s);
+/* Row shards: the front of the solver workspace (every gathered vector and
+ * the exchange mailbox) is written by the peers; its layout is identical on
+ * every rank.  After every rank's aqp_solver_create has returned (host
+ * barrier), pass each rank's mapping of its peers' workspace bases
+ * (peer_bases[rank] = this workspace; CUDA IPC mappings across processes,
+ * plain pointers for ranks sharing a device).  Builds the window graph.
+ * From then on every aqp_solver_* call is collective: all ranks make the
+ * same calls in the same order. */
+int aqp_solver_exchange_region(aqp_solver *s, void **base, size_t *bytes);
+int aqp_solver_connect(aqp_solver *s, void *const *peer_bases, int nranks);
 /* x0 = clamp(0), y0 = 0, all round/anchor buffers <- (x0, y0) (engine.py:174-204) */
 int aqp_solver_init(aqp_solver *s, const aqp_scalars *sc);
 int aqp_solver_set_scalars(aqp_solver *s, const aqp_scalars *sc);
@@ -249,6 +272,12 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
  * pass, 1 vector pass, 2/3 fold-kernel start/end.  Copies up to `cap` pairs
  * (2*cap words) and resets the ring. */
 int aqp_solver_trace(aqp_solver *s, unsigned long long *host_out, int64_t cap, int64_t *count);
+
+/* CUDA IPC of a device buffer (the allocation holding dev_ptr + the offset
+ * of dev_ptr in it); handles are 64 bytes. */
+int aqp_ipc_get_handle(const void *dev_ptr, void *handle64, size_t *offset);
+int aqp_ipc_open(const void *handle64, size_t offset, void **dev_ptr);
+int aqp_ipc_close(void *dev_ptr, size_t offset);
 
 #ifdef __cplusplus
 }

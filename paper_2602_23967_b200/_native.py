@@ -22,6 +22,11 @@ c_double_p = C.POINTER(C.c_double)
 c_int64_p = C.POINTER(C.c_int64)
 
 
+class Shard(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("n0", C.c_int64), ("n1", C.c_int64),
+                ("m0", C.c_int64), ("m1", C.c_int64)]
+
+
 class ProblemDesc(C.Structure):
     _fields_ = [
         ("n", C.c_int64), ("m", C.c_int64),
@@ -120,6 +125,13 @@ SIGNATURES = {
     "aqp_solver_estimate_norm": (C.c_int, [_P, _P, C.c_int, c_double_p, C.POINTER(C.c_int)]),
     "aqp_solver_time_kernel": (C.c_int, [_P, C.c_int, C.c_int, _P, C.c_size_t, c_double_p]),
     "aqp_solver_trace": (C.c_int, [_P, _P, _I64, c_int64_p]),
+    # row shards (multi-GPU)
+    "aqp_problem_shard": (C.c_int, [_P, C.POINTER(Shard)]),
+    "aqp_solver_exchange_region": (C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_size_t)]),
+    "aqp_solver_connect": (C.c_int, [_P, C.POINTER(_P), C.c_int]),
+    "aqp_ipc_get_handle": (C.c_int, [_P, _P, C.POINTER(C.c_size_t)]),
+    "aqp_ipc_open": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
+    "aqp_ipc_close": (C.c_int, [_P, C.c_size_t]),
 }
 
 _lib = None

@@ -151,10 +151,136 @@ __device__ __forceinline__ void block_reduce(RedVals<NS, NM> &v, double *smem /*
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- row shards over peer memory
+// Multi-GPU: rank r owns rows [n0,n1) of A' and Q (x side)
+// and rows [m0,m1) of A (y side).  Every vector that an SpMV gathers is kept
+// full-length on every rank; the kernel that produces a rank's slice stores
+// it locally AND into the same offset of every peer's copy (NVLink P2P
+// stores into the peers' solver workspaces, whose exchange regions have the
+// identical layout on every rank, so peer address = local address +
+// delta[k]).  Reductions and barriers are one-block mailbox exchanges: each
+// rank writes its block-folded partials into mail[epoch & 1][rank] of every
+// peer, then releases flag[rank] = epoch on every peer and acquires all
+// flags >= epoch; every rank then combines the P partials in rank order, so
+// all ranks hold bitwise-identical scalars and take identical branches (the
+// CUDA-graph conditionals included).  No NCCL call sits on the data path.
+constexpr int kMaxRanks = 8;
+
+struct CommBlock {
+  unsigned long long flag[kMaxRanks];  // flag[k]: last epoch rank k arrived at (written by rank k)
+  unsigned long long epoch;            // this rank's exchange counter (device-owned)
+  unsigned long long err;              // epoch of an exchange whose wait timed out (0 = none)
+  unsigned long long pad[6];
+  double mail[2][kMaxRanks][kMaxRed];
+};
+
+struct Comm {
+  int rank = 0, nranks = 1;
+  CommBlock *cb = nullptr;
+  unsigned long long timeout_ns = 30000000000ull;  // a peer that never arrives: give up, flag, carry on
+  long long delta[kMaxRanks] = {};  // byte offset local -> rank k's mapping of the same buffer
+};
+
+template <class T>
+__device__ __forceinline__ T *peer_addr(const Comm &c, T *p, int k) {
+  return reinterpret_cast<T *>(reinterpret_cast<char *>(p) + c.delta[k]);
+}
+
+// store `val` at p[i] on every peer (the local store is the caller's)
+__device__ __forceinline__ void peer_put(const Comm &c, double *p, int64_t i, double val) {
+  for (int k = 0; k < c.nranks; ++k)
+    if (k != c.rank) peer_addr(c, p, k)[i] = val;
+}
+
+__device__ __forceinline__ unsigned long long global_ns_() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Block-wide (every thread of the block calls it): all-reduce of thread 0's
+// `a` over the ranks, combined in rank order; result in thread 0.  With NS =
+// NM = 0 it is a pure barrier.  No-op for one rank.
+template <int NS, int NM>
+__device__ __forceinline__ void comm_allreduce(RedVals<NS, NM> &a, const Comm &c) {
+  if (c.nranks <= 1) return;
+  constexpr int NT = NS + NM;
+  constexpr int NTA = NT > 0 ? NT : 1;
+  __shared__ unsigned long long s_epoch;
+  __shared__ double s_mine[NTA];
+  __shared__ double s_all[kMaxRanks * NTA];
+  if (threadIdx.x == 0) {
+    const unsigned long long e = c.cb->epoch + 1;
+    c.cb->epoch = e;
+    s_epoch = e;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) s_mine[i] = a.s[i];
+#pragma unroll
+    for (int i = 0; i < NM; ++i) s_mine[NS + i] = a.m[i];
+  }
+  __syncthreads();
+  const unsigned long long e = s_epoch;
+  const int P = c.nranks;
+  if (NT > 0) {
+    for (int t = threadIdx.x; t < P * NT; t += blockDim.x) {
+      const int k = t / NTA, i = t % NTA;
+      *peer_addr(c, &c.cb->mail[e & 1][c.rank][i], k) = s_mine[i];
+    }
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < P) {
+    __threadfence_system();
+    st_release_sys(peer_addr(c, &c.cb->flag[c.rank], (int)threadIdx.x), e);
+    // bounded wait: a lost peer must not hang the GPU; the host turns the
+    // recorded epoch into a DeviceError at its next sync (aqp_solver_*)
+    const unsigned long long t0 = global_ns_();
+    const bool broken = *(volatile unsigned long long *)&c.cb->err != 0;  // fail fast after a loss
+    while (!broken && ld_acquire_sys(&c.cb->flag[threadIdx.x]) < e) {
+      __nanosleep(64);
+      if (global_ns_() - t0 > c.timeout_ns) {
+        atomicCAS(&c.cb->err, 0ull, e);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (NT > 0) {
+    for (int t = threadIdx.x; t < P * NT; t += blockDim.x) {
+      const int k = t / NTA, i = t % NTA;
+      s_all[t] = __ldcv(&c.cb->mail[e & 1][k][i]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int i = 0; i < NS; ++i) {
+        double v = s_all[i];
+        for (int k = 1; k < P; ++k) v += s_all[k * NTA + i];
+        a.s[i] = v;
+      }
+#pragma unroll
+      for (int i = 0; i < NM; ++i) {
+        double v = s_all[NS + i];
+        for (int k = 1; k < P; ++k) v = nanmax(v, s_all[k * NTA + NS + i]);
+        a.m[i] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Grid-level epilogue: see grid_end / fin_op in aqp_kernels.cuh.
 struct GridRed {
   double *partials;     // >= kMaxRed * gridDim.x doubles, layout [slot][block]
   unsigned int *ticket;  // zero between launches (reset by the last block)
+  Comm comm;            // row shards: grid totals are all-reduced over the ranks
   // optional device trace (AQP_TRACE=1): (tag, globaltimer ns) pairs
   unsigned long long *trace = nullptr;
   unsigned int *trace_n = nullptr;
@@ -203,6 +329,7 @@ struct DevCsr {
   unsigned int *seg_ticket = nullptr;  // nlongseg counters
   int smem_bytes = 0;                  // dynamic shared memory per block (WARP items only)
   int uniform = 0;                     // every item is THREAD over rows [256 b, 256 b + 256)
+  int row_off = 0;                     // global index of local row 0 (row shards of a symmetric Q)
 };
 
 }  // namespace aqp

@@ -55,4 +55,7 @@ struct aqp_problem {
   int8_t *cone_r = nullptr, *recc_x = nullptr, *cone_y = nullptr, *recc_s = nullptr;
   int *bad = nullptr;
   aqp_problem_info info{};
+  // row shard (aqp_problem_shard): rows [n0,n1) of A' / Q, [m0,m1) of A
+  int rank = 0, nranks = 1;
+  int64_t n0 = 0, n1 = 0, m0 = 0, m1 = 0;
 };

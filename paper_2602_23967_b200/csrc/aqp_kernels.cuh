@@ -137,6 +137,7 @@ __device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *
   if (!last) return false;
   RedVals<NS, NM> a;
   fold_partials<NS, NM>(a, g.partials, gridDim.x, smem);
+  comm_allreduce<NS, NM>(a, g.comm);
   v = a;
   if (threadIdx.x == 0) *g.ticket = 0u;
   return threadIdx.x == 0;
@@ -145,11 +146,17 @@ __device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *
 #ifndef AQP_SPMV_MIN_BLOCKS
 #define AQP_SPMV_MIN_BLOCKS 4
 #endif
+#ifndef AQP_GATHER_BATCH
+#define AQP_GATHER_BATCH 4
+#endif
+#ifndef AQP_UNIFORM_MIN_BLOCKS
+#define AQP_UNIFORM_MIN_BLOCKS 4
+#endif
 // UNIFORM: the plan is all THREAD items over [256 b, 256 b + 256) (the common
 // case of short-row matrices, e.g. every C2 pass); the instantiation then
 // carries only the thread-per-row path, which needs far fewer registers
 template <class Op, bool UNIFORM = false>
-__global__ void __launch_bounds__(kThreads, UNIFORM ? 5 : AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
+__global__ void __launch_bounds__(kThreads, UNIFORM ? AQP_UNIFORM_MIN_BLOCKS : AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
   constexpr int NS = Op::NS, NM = Op::NM;
   // static matrix data first: the plan item does not depend on the predecessor
   PlanItem it;
@@ -183,12 +190,39 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? 5 : AQP_SPMV_MIN_BLOCKS) s
       RowIn rin{};
       if constexpr (RowInOf<Op>::value) rin = o.load_row(r);
       const int b = __ldg(M.ptr + r), e = __ldg(M.ptr + r + 1);
+      const int rg = r + M.row_off;  // global row (diagonal position of a symmetric shard)
       double lo = 0.0, up = 0.0;
+#if AQP_GATHER_BATCH > 1
+      // the row's nonzeros in chunks of AQP_GATHER_BATCH: all index/value
+      // loads of a chunk, then all its gathers, then the sums in column
+      // order (bitwise the sequential loop) -- two dependent round trips per
+      // chunk instead of two per nonzero
+      for (int k = b; k < e; k += AQP_GATHER_BATCH) {
+        int cc[AQP_GATHER_BATCH];
+        double pv[AQP_GATHER_BATCH];
+#pragma unroll
+        for (int u = 0; u < AQP_GATHER_BATCH; ++u) {
+          const bool in = k + u < e;
+          cc[u] = in ? __ldg(M.idx + k + u) : 0;
+          pv[u] = in ? __ldg(M.val + k + u) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < AQP_GATHER_BATCH; ++u)
+          if (k + u < e) pv[u] = pv[u] * o.gather(cc[u]);
+#pragma unroll
+        for (int u = 0; u < AQP_GATHER_BATCH; ++u) {
+          if (k + u < e) {
+            if (Op::SYM && cc[u] < rg) lo += pv[u]; else up += pv[u];
+          }
+        }
+      }
+#else
       for (int k = b; k < e; ++k) {
         const int c = __ldg(M.idx + k);
         const double p = __ldg(M.val + k) * o.gather(c);
-        if (Op::SYM && c < r) lo += p; else up += p;
+        if (Op::SYM && c < rg) lo += p; else up += p;
       }
+#endif
       const double val = Op::SYM ? lo + up : up;
       if constexpr (RowInOf<Op>::value) o.row_in(r, val, rin, acc); else o.row(r, val, acc);
     }
@@ -217,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? 5 : AQP_SPMV_MIN_BLOCKS) s
       const int b = __ldg(M.ptr + r) - k0, e = __ldg(M.ptr + r + 1) - k0;
       double lo = 0.0, up = 0.0;
       for (int j = b + lane; j < e; j += 32) {
-        if (Op::SYM && scol[j] < r) lo += sprod[j]; else up += sprod[j];
+        if (Op::SYM && scol[j] < r + M.row_off) lo += sprod[j]; else up += sprod[j];
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
@@ -233,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? 5 : AQP_SPMV_MIN_BLOCKS) s
       for (int k = it.k0; k < it.k1; ++k) {
         const int c = __ldg(M.idx + k);
         const double p = __ldg(M.val + k) * o.gather(c);
-        if (Op::SYM && c < r) lo += p; else up += p;
+        if (Op::SYM && c < r + M.row_off) lo += p; else up += p;
       }
       o.row(r, Op::SYM ? lo + up : up, acc);
     }
@@ -246,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? 5 : AQP_SPMV_MIN_BLOCKS) s
     for (int k = it.k0 + threadIdx.x; k < it.k1; k += kThreads) {
       const int c = __ldg(M.idx + k);
       const double p = __ldg(M.val + k) * o.gather(c);
-      if (Op::SYM && c < r) lu.s[0] += p; else lu.s[1] += p;
+      if (Op::SYM && c < r + M.row_off) lu.s[0] += p; else lu.s[1] += p;
     }
     block_reduce<2, 0>(lu, sred);
     if (it.nseg == 1) {
@@ -303,16 +337,43 @@ template <class Op>
 __global__ void __launch_bounds__(kThreads) fin_op(Op op, GridRed g, unsigned nb) {
   constexpr int NS = Op::NS, NM = Op::NM;
   pdl_wait();
-  pdl_trigger();  // one block: let the next kernel's blocks get resident now
+  // one block: let the next kernel's blocks get resident now -- unless this
+  // block waits on peers (row shards), whose dependents must not occupy SMs
+  // while it spins
+  const bool shard = g.comm.nranks > 1;
+  if (!shard) pdl_trigger();
   trace_mark(g, 2);
-  if (op.skip()) return;
+  if (op.skip()) {
+    pdl_trigger();
+    return;
+  }
   Op o = op;
   o.prepare();
   __shared__ double sred[kWarps * kMaxRed];
   RedVals<NS, NM> a;
   fold_partials<NS, NM>(a, g.partials, nb, sred);
+  comm_allreduce<NS, NM>(a, g.comm);
+  if (shard) pdl_trigger();
   if (threadIdx.x == 0) o.finalize(a);
   trace_mark(g, 3);
+}
+
+// barrier over the ranks (a zero-width exchange); one block
+static __global__ void k_comm_barrier(GridRed g) {
+  pdl_wait();
+  RedVals<0, 0> a;
+  comm_allreduce<0, 0>(a, g.comm);
+  pdl_trigger();
+}
+
+// replicate this rank's slice [0, len) of a gathered vector (pointer already
+// offset to the slice) into every peer's copy
+static __global__ void __launch_bounds__(kThreads) k_comm_push(const double *p, int64_t len, GridRed g) {
+  pdl_wait();
+  const Comm &c = g.comm;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    peer_put(c, const_cast<double *>(p), i, p[i]);
+  pdl_trigger();
 }
 
 // grid of an elementwise pass: a pure function of n (so reductions are

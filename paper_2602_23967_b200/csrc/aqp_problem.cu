@@ -505,6 +505,8 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
   p->ctx = ctx;
   p->n = d->n;
   p->m = d->m;
+  p->n1 = d->n;
+  p->m1 = d->m;
   p->quad_kind = d->quad_kind;
   Bump b;
   b.base = persistent;
@@ -596,6 +598,47 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
   p->info.q_items = p->Q.nitems;
   p->info.persistent_bytes = b.used;
   *out = p;
+  return AQP_OK;
+}
+
+// Restrict the SpMV passes to rows [r0, r1) of M: the row pointers are a
+// window of the full array (absolute nonzero offsets, so idx/val stay put)
+// and the work plan is rebuilt for the local rows.
+static int slice_rows(aqp_ctx *ctx, DevCsr &M, CsrStore &s, int64_t r0, int64_t r1, int row_off) {
+  std::vector<int> hptr((size_t)(r1 - r0 + 1));
+  AQP_CUDA(cudaMemcpyAsync(hptr.data(), M.ptr + r0, hptr.size() * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  AQP_CUDA(cudaStreamSynchronize(ctx->stream));
+  M.ptr += r0;
+  M.rows = (int)(r1 - r0);
+  M.nnz = (int64_t)hptr.back() - hptr.front();
+  M.row_off = row_off;
+  AQP_CUDA(cudaMemsetAsync(s.seg_ticket, 0, s.seg_cap * sizeof(unsigned), ctx->stream));
+  return finish_plan(ctx, M, hptr.data(), nullptr, false, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap);
+}
+
+int aqp_problem_shard(aqp_problem *p, const aqp_shard *sh) {
+  if (!p || !sh) return fail(AQP_EINVAL, "NULL argument");
+  if (p->nranks > 1 || p->n0 || p->m0 || p->n1 != p->n || p->m1 != p->m)
+    return fail(AQP_ESTATE, "problem is already sharded");
+  if (sh->nranks < 1 || sh->nranks > kMaxRanks || sh->rank < 0 || sh->rank >= sh->nranks)
+    return fail(AQP_EINVAL, "rank / nranks out of range (at most 8 ranks)");
+  if (sh->n0 < 0 || sh->n1 > p->n || sh->n0 >= sh->n1 || sh->m0 < 0 || sh->m1 > p->m || sh->m0 >= sh->m1)
+    return fail(AQP_EINVAL, "shard row ranges must be non-empty and inside [0,n) / [0,m)");
+  if (sh->nranks > 1 && p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK)
+    return fail(AQP_EINVAL, "low-rank Q is not row-sharded (R x needs every column)");
+  AQP_CUDA(cudaSetDevice(p->ctx->device));
+  AQP_TRY(slice_rows(p->ctx, p->A, p->sA, sh->m0, sh->m1, 0));
+  AQP_TRY(slice_rows(p->ctx, p->At, p->sAt, sh->n0, sh->n1, 0));
+  if (p->quad_kind == AQP_QUAD_SPARSE) AQP_TRY(slice_rows(p->ctx, p->Q, p->sQ, sh->n0, sh->n1, (int)sh->n0));
+  p->rank = sh->rank;
+  p->nranks = sh->nranks;
+  p->n0 = sh->n0;
+  p->n1 = sh->n1;
+  p->m0 = sh->m0;
+  p->m1 = sh->m1;
+  p->info.a_items = p->A.nitems;
+  p->info.at_items = p->At.nitems;
+  p->info.q_items = p->Q.nitems;
   return AQP_OK;
 }
 

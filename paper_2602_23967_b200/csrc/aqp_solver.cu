@@ -75,6 +75,10 @@ struct SV {
   double eps_tol, gamma, tol_scale, tol_floor, diag_bound;
   int adaptive, max_inner, halpern, quad_kind;
   int64_t n, m;
+  // row shards: vector pointers above are offset to this rank's slice
+  // (x side by xoff, y side by yoff); gathers index the full copies
+  int64_t xoff, yoff, nl, ml;
+  Comm cm;
   cudaGraphConditionalHandle bb_cond, outer_cond;
   int in_graph;  // 0 for stand-alone launches (kernel timing): no conditional updates
 };
@@ -146,7 +150,7 @@ struct OpP1Bb {
   // every block's first memory access behind a round trip
   __device__ bool skip() const { return false; }
   __device__ void prepare() {
-    y = pick3(v.ys, v.ctrl->ycur);
+    y = pick3(v.ys, v.ctrl->ycur) - v.yoff;
     x = pick3(v.xs, v.ctrl->xcur);
   }
   __device__ double gather(int c) const { return __ldg(y + c); }
@@ -156,7 +160,9 @@ struct OpP1Bb {
   __device__ RowIn load_row(int r) const { return RowIn{v.c[r], x[r], v.vlo[r], v.vhi[r]}; }
   __device__ void row_in(int r, double s, const RowIn &in, RedVals<0, 0> &) const {
     v.lin[r] = in.c + s;                            // engine.py:214 cost + A'y
-    v.xbb[0][r] = clip(in.x, in.lo, in.hi);           // inner.py:94
+    const double x0 = clip(in.x, in.lo, in.hi);       // inner.py:94
+    v.xbb[0][r] = x0;
+    peer_put(v.cm, v.xbb[0], r, x0);                  // G0 gathers x0 on every rank
   }
   __device__ void row(int r, double s, RedVals<0, 0> &acc) const { row_in(r, s, load_row(r), acc); }
   __device__ void finalize(const RedVals<0, 0> &) const {}
@@ -178,7 +184,7 @@ struct OpP1Diag {
   __device__ bool skip() const { return false; }
   __device__ void prepare() {
     const Ctrl *ct = v.ctrl;
-    y = pick3(v.ys, ct->ycur);
+    y = pick3(v.ys, ct->ycur) - v.yoff;
     x = pick3(v.xs, ct->xcur);
     xprev = pick3(v.xs, ct->xprev);
     znew = pick3(v.xs, 3 - ct->xcur - ct->xprev);
@@ -190,7 +196,9 @@ struct OpP1Diag {
     const double lin = v.c[r] + s;
     const double xk = x[r];
     const double xp = clip((xk - tau * lin) / (1.0 + tau * v.qd[r]), v.vlo[r], v.vhi[r]);  // _core.pyx:127
-    v.xbar[r] = 2.0 * xp + (-1.0) * xk;                                                     // axpby
+    const double xb = 2.0 * xp + (-1.0) * xk;                                               // axpby
+    v.xbar[r] = xb;
+    peer_put(v.cm, v.xbar, r, xb);
     const double z = cb(xp, v.anc_x, xprev, r);
     const double d = z - xk;
     acc.s[0] += d * d;
@@ -227,7 +235,7 @@ struct OpGrad {
     cen = pick3(v.xs, ct->xcur);
     tau = ct->tau;
   }
-  __device__ double gather(int c) const { return __ldg(xt + c); }
+  __device__ double gather(int c) const { return __ldg(xt - v.xoff + c); }
   // epilogue operands of row r, loaded ahead of the SpMV tile (THREAD tiles)
   struct RowIn {
     double x, c, l, lo, hi, xo, go, rt;
@@ -349,7 +357,11 @@ struct OpStep {
     xn = pick3(v.xbb, ct->bb_new);
     alpha = ct->alpha;
   }
-  __device__ void elem(int64_t i, RedVals<0, 0> &) const { xn[i] = clip(xo[i] - alpha * go[i], v.vlo[i], v.vhi[i]); }
+  __device__ void elem(int64_t i, RedVals<0, 0> &) const {
+    const double x = clip(xo[i] - alpha * go[i], v.vlo[i], v.vhi[i]);
+    xn[i] = x;
+    peer_put(v.cm, xn, i, x);  // the next G pass gathers x_t on every rank
+  }
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
 
@@ -375,7 +387,9 @@ struct OpXPost {
   }
   __device__ void elem(int64_t i, RedVals<1, 0> &acc) const {
     const double p = xp[i], xk = x[i];
-    v.xbar[i] = 2.0 * p + (-1.0) * xk;
+    const double xb = 2.0 * p + (-1.0) * xk;
+    v.xbar[i] = xb;
+    peer_put(v.cm, v.xbar, i, xb);
     const double z = cb(p, v.anc_x, xprev, (int)i);
     const double d = z - xk;
     acc.s[0] += d * d;
@@ -406,7 +420,7 @@ struct OpP2 {
     sigma = ct->sigma;
     cb.init(v);
   }
-  __device__ double gather(int c) const { return halted ? 0.0 : __ldg(v.xbar + c); }
+  __device__ double gather(int c) const { return halted ? 0.0 : __ldg(v.xbar - v.xoff + c); }
   struct RowIn {
     double y, lo, hi, anc, blk, prev;
   };
@@ -431,6 +445,7 @@ struct OpP2 {
     }
     v.yblk[r] = in.blk + z;
     ynew[r] = z;
+    peer_put(v.cm, ynew, r, z);  // the next P1 gathers y on every rank
   }
   __device__ void row(int r, double s, RedVals<0, 0> &acc) const { row_in(r, s, load_row(r), acc); }
   __device__ void finalize(const RedVals<0, 0> &) const {
@@ -461,6 +476,7 @@ struct OpRx {
   __device__ void prepare() {
     const Ctrl *ct = v.ctrl;
     x = src == 0 ? pick3(v.xbb, 0) : src == 1 ? pick3(v.xbb, ct->bb_new) : src == 2 ? v.xeval : pick2(v.dx, src - 3);
+    x -= v.xoff;
   }
   __device__ double gather(int c) const { return __ldg(x + c); }
   __device__ void row(int r, double s, RedVals<0, 0> &) const { v.rx[r] = s; }
@@ -594,7 +610,7 @@ struct OpChkA {
       ok[j] = rays && cand_valid(ct, j, nrm[j]);
     }
   }
-  __device__ double gather(int c) const { return __ldg(v.xeval + c); }
+  __device__ double gather(int c) const { return __ldg(v.xeval - v.xoff + c); }
   __device__ void row(int r, double s, RedVals<6, 1> &acc) const {
     acc.m[0] = nanmax(acc.m[0], absd(s - clip(s, v.clo[r], v.chi[r])));
 #pragma unroll
@@ -632,7 +648,8 @@ struct OpStore {
   __device__ bool skip() const { return src >= 2 && v.ctrl->pw_stop; }
   __device__ void prepare() {
     const Ctrl *ct = v.ctrl;
-    x = src == 0 ? v.xeval : src == 1 ? pick3(v.ys, ct->ycur) : src == 2 ? pick3(v.xbb, 1) : v.tm;
+    x = src == 0 ? v.xeval - v.xoff : src == 1 ? pick3(v.ys, ct->ycur) - v.yoff
+        : src == 2 ? pick3(v.xbb, 1) - v.xoff : v.tm - v.yoff;
     out = dst == 0 ? v.qx : dst == 1 ? v.aty : dst == 2 ? v.tm : pick3(v.xbb, 2);
   }
   __device__ double gather(int c) const { return __ldg(x + c); }
@@ -724,7 +741,7 @@ struct OpChkYRay {
     const Ctrl *ct = v.ctrl;
     return !cand_valid(ct, j, ct->red[R_YR + 9 * j]);
   }
-  __device__ void prepare() { ray = pick2(v.dy, j); }
+  __device__ void prepare() { ray = pick2(v.dy, j) - v.yoff; }
   __device__ double gather(int c) const { return __ldg(ray + c); }
   __device__ void row(int r, double s, RedVals<3, 2> &acc) const {
     const double p = cone_proj(s, v.cone_r[r]);
@@ -758,7 +775,7 @@ struct OpChkXRay {
     return !(cand_valid(ct, j, xr[0]) && xr[1] < -v.eps_tol);
   }
   __device__ void prepare() { d = pick2(v.dx, j); }
-  __device__ double gather(int c) const { return __ldg(d + c); }
+  __device__ double gather(int c) const { return __ldg(d - v.xoff + c); }
   __device__ void row(int r, double s, RedVals<0, 1> &acc) const {
     if (which == 0) {
       acc.m[0] = nanmax(acc.m[0], absd(s - cone_proj(s, v.recc_s[r])));
@@ -830,6 +847,35 @@ struct OpState {
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
 
+// row shards: replicate this rank's slice of a gathered vector into every
+// peer's copy (cold paths; the hot producers store to the peers directly)
+struct OpPush {
+  static constexpr int NS = 0, NM = 0;
+  static constexpr bool FINAL = false;
+  SV v;
+  int which;  // PushBuf
+  double *p;
+  __device__ bool skip() const { return false; }
+  __device__ void prepare() {
+    const Ctrl *ct = v.ctrl;
+    switch (which) {
+      case 0: p = pick3(v.ys, ct->ycur); break;
+      case 1: p = v.xeval; break;
+      case 2: p = v.dy[0]; break;
+      case 3: p = v.dy[1]; break;
+      case 4: p = v.dx[0]; break;
+      case 5: p = v.dx[1]; break;
+      case 6: p = pick3(v.xbb, 1); break;
+      case 7: p = v.tm; break;
+      case 8: p = v.rs; break;
+      default: p = pick3(v.xs, ct->xcur); break;
+    }
+  }
+  __device__ void elem(int64_t i, RedVals<0, 0> &) const { peer_put(v.cm, p, i, p[i]); }
+  __device__ void finalize(const RedVals<0, 0> &) const {}
+};
+enum PushBuf : int { PB_Y = 0, PB_XEVAL, PB_DY0, PB_DY1, PB_DX0, PB_DX1, PB_PW, PB_TM, PB_RS, PB_X };
+
 // ---------------------------------------------------------------- power iteration ops
 struct OpPwNorm {  // sum of squares of xbb[idx] -> red[slot]
   static constexpr int NS = 1, NM = 0;
@@ -879,14 +925,22 @@ __global__ void __launch_bounds__(kFinThreads) fin_ctrl_op(Op op, GridRed g, uns
   __shared__ unsigned long long cbuf[W];
   __shared__ double sred[(kFinThreads / 32) * kMaxRed];
   pdl_wait();
-  pdl_trigger();
+  // row shards: this block waits on its peers, so its dependents must not be
+  // made resident (and occupy SMs other ranks' kernels need) before that
+  const bool shard = g.comm.nranks > 1;
+  if (!shard) pdl_trigger();
   trace_mark(g, 2);
-  if (op.skip()) return;
+  if (op.skip()) {
+    pdl_trigger();
+    return;
+  }
   Ctrl *gctrl = op.v.ctrl;
   const unsigned long long *src = reinterpret_cast<const unsigned long long *>(gctrl);
   for (int i = threadIdx.x; i < W; i += blockDim.x) cbuf[i] = __ldcg(src + i);
   RedVals<NS, NM> a;
   fold_partials<NS, NM>(a, g.partials, nb, sred);  // ends with __syncthreads
+  comm_allreduce<NS, NM>(a, g.comm);               // all ranks: identical totals
+  if (shard) pdl_trigger();
   trace_mark(g, 4);
   Op o = op;
   o.v.ctrl = reinterpret_cast<Ctrl *>(cbuf);
@@ -917,6 +971,20 @@ struct aqp_solver {
   int64_t kernel_launches = 0;
   bool eager = false;
   bool pdl = false;
+  void *ws_base = nullptr;  // workspace (its front is the peer-visible exchange region)
+  // pinned host staging: every host<->device copy of the solver is a true
+  // async copy (pageable copies serialise on the driver's staging buffer,
+  // which can stall one rank's launches behind another rank's pending read)
+  struct Pinned {
+    Ctrl pull;                    // control-block reads
+    Ctrl ring[32];                // host -> device scalar pushes (reused after a sync)
+    unsigned long long err;       // exchange error word
+    int flag;                     // eager-mode flag reads
+  } *pin = nullptr;
+  unsigned ring_i = 0;
+  double *bounce = nullptr;       // vector reads / start-vector upload
+  static constexpr size_t kBounce = 1 << 21;  // doubles (16 MB)
+  bool shard = false;       // problem is row-sharded (nranks > 1): graph built at connect
 };
 
 namespace {
@@ -941,6 +1009,10 @@ void layout_solver(Bump &b, aqp_problem *p, SV &v, Ctrl **ctrl, GridRed &gr) {
   v.dy[0] = vm(); v.dy[1] = vm();
   v.tm = vm();
   *ctrl = (Ctrl *)b.take(sizeof(Ctrl));
+  // everything above has the same offsets on every rank (sizes depend on the
+  // global n, m only): the peer-visible exchange region.  Partials below are
+  // sized by this rank's plan.
+  gr.comm.cb = (CommBlock *)b.take(sizeof(CommBlock));
   int64_t maxg = 148 * 8;
   for (const DevCsr *M : {&p->A, &p->At, &p->Q, &p->R, &p->Rt}) maxg = std::max<int64_t>(maxg, M->nitems);
   gr.partials = (double *)b.take(maxg * kMaxRed * 8);
@@ -1019,6 +1091,12 @@ cudaError_t node_elem_fin(cudaGraph_t g, GNode &last, int64_t n, const Op &op, G
   cudaError_t e = add_node(g, last, (unsigned)elem_grid(n), elem_op<Op>, n, op, gr);
   if (e != cudaSuccess) return e;
   return add_node_cfg(g, last, 1u, (unsigned)kFinThreads, 0u, fin_ctrl_op<Op>, op, gr, (unsigned)elem_grid(n));
+}
+
+// row shards: a one-block exchange after a producer whose output the next
+// node gathers (the peers' stores must have landed)
+cudaError_t node_barrier(cudaGraph_t g, GNode &last, GridRed gr) {
+  return add_node_cfg(g, last, 1u, 32u, 0u, k_comm_barrier, gr);
 }
 
 template <class Op>
@@ -1101,6 +1179,10 @@ int build_graph(aqp_solver *s) {
     OpP1Bb o{};
     o.v = v;
     AQP_CUDA(node_spmv(body, last, p->At, o, gr));
+    if (s->shard) {
+      AQP_CUDA(node_barrier(body, last, gr));
+      fixed += 1;
+    }
     if (lowrank) AQP_TRY(add_lowrank(s, body, last, 0));
     OpGrad<true> g0{};
     g0.v = v;
@@ -1120,14 +1202,15 @@ int build_graph(aqp_solver *s) {
     GNode il;
     OpStep st{};
     st.v = v;
-    AQP_CUDA(node_elem(ib, il, p->n, st, gr));
+    AQP_CUDA(node_elem(ib, il, v.nl, st, gr));
+    if (s->shard) AQP_CUDA(node_barrier(ib, il, gr));
     if (lowrank) AQP_TRY(add_lowrank(s, ib, il, 1));
     OpGrad<false> gg{};
     gg.v = v;
     AQP_CUDA(node_spmv_fin(ib, il, p->Q, gg, gr));
     OpXPost xp{};
     xp.v = v;
-    AQP_CUDA(node_elem_fin(body, last, p->n, xp, gr));
+    AQP_CUDA(node_elem_fin(body, last, v.nl, xp, gr));
     fixed += 2;
   }
   OpP2 p2{};
@@ -1163,14 +1246,18 @@ int build_graph_any(aqp_solver *s) {
 int push_scalars(aqp_solver *s) {
   s->h.tau = s->h.s.eta / s->h.s.omega;    // engine.py:148-150
   s->h.sigma = s->h.s.eta * s->h.s.omega;  // engine.py:152-154
-  AQP_CUDA(cudaMemcpyAsync(s->d_ctrl, &s->h, offsetof(Ctrl, xcur), cudaMemcpyHostToDevice, s->p->ctx->stream));
+  Ctrl *slot = &s->pin->ring[s->ring_i++ % 32];
+  std::memcpy(slot, &s->h, offsetof(Ctrl, xcur));
+  AQP_CUDA(cudaMemcpyAsync(s->d_ctrl, slot, offsetof(Ctrl, xcur), cudaMemcpyHostToDevice, s->p->ctx->stream));
   return AQP_OK;
 }
 
 template <class T>
 int poke(aqp_solver *s, T Ctrl::*field, T value) {
   s->h.*field = value;
-  AQP_CUDA(cudaMemcpyAsync(&(s->d_ctrl->*field), &(s->h.*field), sizeof(T), cudaMemcpyHostToDevice,
+  Ctrl *slot = &s->pin->ring[s->ring_i++ % 32];
+  slot->*field = value;
+  AQP_CUDA(cudaMemcpyAsync(&(s->d_ctrl->*field), &(slot->*field), sizeof(T), cudaMemcpyHostToDevice,
                            s->p->ctx->stream));
   return AQP_OK;
 }
@@ -1179,15 +1266,39 @@ int poke(aqp_solver *s, T Ctrl::*field, T value) {
 int push_all(aqp_solver *s) {
   s->h.tau = s->h.s.eta / s->h.s.omega;
   s->h.sigma = s->h.s.eta * s->h.s.omega;
-  AQP_CUDA(cudaMemcpyAsync(s->d_ctrl, &s->h, sizeof(Ctrl), cudaMemcpyHostToDevice, s->p->ctx->stream));
+  Ctrl *slot = &s->pin->ring[s->ring_i++ % 32];
+  *slot = s->h;
+  AQP_CUDA(cudaMemcpyAsync(s->d_ctrl, slot, sizeof(Ctrl), cudaMemcpyHostToDevice, s->p->ctx->stream));
   AQP_CUDA(cudaStreamSynchronize(s->p->ctx->stream));
   return AQP_OK;
 }
 
 int pull_ctrl(aqp_solver *s) {
   cudaStream_t st = s->p->ctx->stream;
-  AQP_CUDA(cudaMemcpyAsync(&s->h, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaMemcpyAsync(&s->pin->pull, s->d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  s->pin->err = 0;
+  if (s->shard) AQP_CUDA(cudaMemcpyAsync(&s->pin->err, &s->gr.comm.cb->err, 8, cudaMemcpyDeviceToHost, st));
   AQP_CUDA(cudaStreamSynchronize(st));
+  s->h = s->pin->pull;
+  const unsigned long long err = s->pin->err;
+  if (err)
+    return fail(AQP_ECUDA, "row-shard exchange " + std::to_string(err) + " timed out on rank " +
+                               std::to_string(s->p->rank) + " (a peer stopped arriving)");
+  return AQP_OK;
+}
+
+// row shards: replicate this rank's slice of buffer `which` (PushBuf) into
+// the peers' copies and wait until every rank has done the same
+int push_buf(aqp_solver *s, int which) {
+  if (!s->shard) return AQP_OK;
+  cudaStream_t st = s->p->ctx->stream;
+  const bool yside = which == PB_Y || which == PB_DY0 || which == PB_DY1 || which == PB_TM;
+  OpPush o{};
+  o.v = s->v;
+  o.which = which;
+  AQP_CUDA(run_elem(st, yside ? s->v.ml : s->v.nl, o, s->gr));
+  k_comm_barrier<<<1, 32, 0, st>>>(s->gr);
+  AQP_CUDA(cudaGetLastError());
   return AQP_OK;
 }
 
@@ -1198,8 +1309,10 @@ int state_op(aqp_solver *s, int mode) {
     o.v = s->v;
     o.side = side;
     o.mode = mode;
-    AQP_CUDA(run_elem(st, side == 0 ? s->p->n : s->p->m, o, s->gr));
+    AQP_CUDA(run_elem(st, side == 0 ? s->v.nl : s->v.ml, o, s->gr));
   }
+  // init / rollback rewrite the current y, which the next P1 gathers
+  if (mode == 0 || mode == 3) AQP_TRY(push_buf(s, PB_Y));
   return AQP_OK;
 }
 
@@ -1207,6 +1320,8 @@ int state_op(aqp_solver *s, int mode) {
 
 // ====================================================================== C ABI
 extern "C" {
+
+static int run_eager(aqp_solver *s, int64_t n_iters);
 
 int aqp_solver_sizes(const aqp_problem *p, size_t *workspace_bytes) {
   if (!p || !workspace_bytes) return fail(AQP_EINVAL, "NULL argument");
@@ -1247,6 +1362,28 @@ int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, si
   v.quad_kind = p->quad_kind;
   v.n = p->n;
   v.m = p->m;
+  // row shards (aqp_problem_shard): offset every vector to this rank's slice
+  v.xoff = p->n0;
+  v.yoff = p->m0;
+  v.nl = p->n1 - p->n0;
+  v.ml = p->m1 - p->m0;
+  s->ws_base = ws;
+  s->shard = p->nranks > 1;
+  AQP_CUDA(cudaMallocHost(&s->pin, sizeof(aqp_solver::Pinned)));
+  AQP_CUDA(cudaMallocHost(&s->bounce, aqp_solver::kBounce * 8));
+  if (p->n0 || p->m0) {
+    for (int i = 0; i < 3; ++i) { v.xs[i] += v.xoff; v.ys[i] += v.yoff; v.xbb[i] += v.xoff; }
+    for (int i = 0; i < 2; ++i) { v.gbb[i] += v.xoff; v.dx[i] += v.xoff; v.dy[i] += v.yoff; }
+    for (double **q : {&v.anc_x, &v.xlast, &v.xblk, &v.xavgp, &v.lin, &v.xbar, &v.rtv, &v.xeval, &v.qx, &v.aty, &v.rs})
+      *q += v.xoff;
+    for (double **q : {&v.anc_y, &v.ylast, &v.yblk, &v.yavgp, &v.tm}) *q += v.yoff;
+    v.c += v.xoff; v.vlo += v.xoff; v.vhi += v.xoff; v.qd += v.xoff;
+    v.cone_r += v.xoff; v.recc_x += v.xoff;
+    v.clo += v.yoff; v.chi += v.yoff; v.cone_y += v.yoff; v.recc_s += v.yoff;
+  }
+  s->gr.comm.rank = p->rank;
+  s->gr.comm.nranks = 1;  // until aqp_solver_connect
+  v.cm = s->gr.comm;
   std::memset(&s->h, 0, sizeof(Ctrl));
   s->h.xcur = 0; s->h.xprev = 1; s->h.ycur = 0; s->h.yprev = 1;
   const char *eager = getenv("AQP_EAGER");
@@ -1261,13 +1398,71 @@ int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, si
   }
   cudaStream_t st = p->ctx->stream;
   AQP_CUDA(cudaMemsetAsync(s->gr.ticket, 0, 64, st));
-  int rc = build_graph_any(s);
-  if (rc) {
-    delete s;
-    return rc;
+  AQP_CUDA(cudaMemsetAsync(s->gr.comm.cb, 0, sizeof(CommBlock), st));
+  // the mailbox must be zero before any peer can write to it (the caller
+  // holds a host barrier between every rank's create and the first exchange)
+  AQP_CUDA(cudaStreamSynchronize(st));
+  if (!s->shard) {  // sharded solvers build their graph once the peers are connected
+    int rc = build_graph_any(s);
+    if (rc) {
+      aqp_solver_destroy(s);
+      return rc;
+    }
   }
   *out = s;
   return AQP_OK;
+}
+
+int aqp_solver_exchange_region(aqp_solver *s, void **base, size_t *bytes) {
+  if (!s || !base || !bytes) return fail(AQP_EINVAL, "NULL argument");
+  *base = s->ws_base;
+  *bytes = (size_t)((char *)s->gr.comm.cb - (char *)s->ws_base) + sizeof(CommBlock);
+  return AQP_OK;
+}
+
+int aqp_solver_connect(aqp_solver *s, void *const *peer_bases, int nranks) {
+  if (!s || !peer_bases) return fail(AQP_EINVAL, "NULL argument");
+  aqp_problem *p = s->p;
+  if (nranks != p->nranks) return fail(AQP_EINVAL, "nranks differs from the problem's shard");
+  if (nranks == 1) return peer_bases[0] == s->ws_base ? AQP_OK : fail(AQP_EINVAL, "peer_bases[0] is not this workspace");
+  if (s->exec) return fail(AQP_ESTATE, "solver already connected");
+  Comm c = s->gr.comm;
+  c.nranks = nranks;
+  if (const char *t = getenv("AQP_COMM_TIMEOUT_S")) c.timeout_ns = (unsigned long long)(atof(t) * 1e9);
+  for (int k = 0; k < kMaxRanks; ++k) c.delta[k] = 0;
+  for (int k = 0; k < nranks; ++k) {
+    if (!peer_bases[k]) return fail(AQP_EINVAL, "NULL peer base");
+    c.delta[k] = (long long)((const char *)peer_bases[k] - (const char *)s->ws_base);
+  }
+  if (c.delta[p->rank] != 0) return fail(AQP_EINVAL, "peer_bases[rank] must be this solver's workspace");
+  AQP_CUDA(cudaSetDevice(p->ctx->device));
+  // Load every kernel of the solve now, while this rank still runs alone
+  // (comm not yet enabled: no exchange waits).  With lazy module loading the
+  // first launch of a kernel loads it under a context-wide synchronisation;
+  // ranks that share a device would otherwise deadlock (until the exchange
+  // timeout) when one rank loads a kernel while another spins in an exchange.
+  {
+    std::vector<double> ones((size_t)p->n, 1.0);
+    double est = 0.0;
+    int ann = 0;
+    AQP_TRY(aqp_solver_estimate_norm(s, ones.data(), 1, &est, &ann));
+    aqp_scalars sc{};
+    sc.eta = 1.0;
+    sc.omega = 1.0;
+    sc.inner_tol = 1e-2;
+    AQP_TRY(aqp_solver_init(s, &sc));
+    AQP_TRY(run_eager(s, 1));
+    aqp_check_result cr;
+    AQP_TRY(aqp_solver_check(s, 1, &cr));
+    AQP_TRY(state_op(s, 1));
+    AQP_TRY(state_op(s, 2));
+    AQP_TRY(state_op(s, 3));
+    AQP_TRY(state_op(s, 4));
+    AQP_TRY(pull_ctrl(s));
+  }
+  s->gr.comm = c;
+  s->v.cm = c;
+  return build_graph_any(s);
 }
 
 int aqp_solver_destroy(aqp_solver *s) {
@@ -1276,6 +1471,8 @@ int aqp_solver_destroy(aqp_solver *s) {
   if (s->gr.trace_n) cudaFree(s->gr.trace_n);
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->graph) cudaGraphDestroy(s->graph);
+  if (s->pin) cudaFreeHost(s->pin);
+  if (s->bounce) cudaFreeHost(s->bounce);
   delete s;
   return AQP_OK;
 }
@@ -1335,18 +1532,26 @@ static int run_eager(aqp_solver *s, int64_t n_iters) {
       OpP1Bb o{};
       o.v = v;
       AQP_CUDA(run_spmv(st, p->At, o, gr));
+      if (s->shard) {
+        k_comm_barrier<<<1, 32, 0, st>>>(gr);
+        AQP_CUDA(cudaGetLastError());
+      }
       if (lowrank) AQP_TRY(lowrank_pass(0));
       OpGrad<true> g0{};
       g0.v = v;
       AQP_CUDA(run_spmv_fin(st, p->Q, g0, gr));
       for (;;) {
-        int cont = 0;
-        AQP_CUDA(cudaMemcpyAsync(&cont, &s->d_ctrl->bb_cont, sizeof(int), cudaMemcpyDeviceToHost, st));
+        AQP_CUDA(cudaMemcpyAsync(&s->pin->flag, &s->d_ctrl->bb_cont, sizeof(int), cudaMemcpyDeviceToHost, st));
         AQP_CUDA(cudaStreamSynchronize(st));
+        const int cont = s->pin->flag;
         if (!cont) break;
         OpStep sp{};
         sp.v = v;
-        AQP_CUDA(run_elem(st, p->n, sp, gr));
+        AQP_CUDA(run_elem(st, v.nl, sp, gr));
+        if (s->shard) {
+          k_comm_barrier<<<1, 32, 0, st>>>(gr);
+          AQP_CUDA(cudaGetLastError());
+        }
         if (lowrank) AQP_TRY(lowrank_pass(1));
         OpGrad<false> gg{};
         gg.v = v;
@@ -1354,14 +1559,14 @@ static int run_eager(aqp_solver *s, int64_t n_iters) {
       }
       OpXPost xp{};
       xp.v = v;
-      AQP_CUDA(run_elem_fin(st, p->n, xp, gr));
+      AQP_CUDA(run_elem_fin(st, v.nl, xp, gr));
     }
     OpP2 p2{};
     p2.v = v;
     AQP_CUDA(run_spmv_fin(st, p->A, p2, gr));
-    int halted = 0;
-    AQP_CUDA(cudaMemcpyAsync(&halted, &s->d_ctrl->s.halted, sizeof(int), cudaMemcpyDeviceToHost, st));
+    AQP_CUDA(cudaMemcpyAsync(&s->pin->flag, &s->d_ctrl->s.halted, sizeof(int), cudaMemcpyDeviceToHost, st));
     AQP_CUDA(cudaStreamSynchronize(st));
+    const int halted = s->pin->flag;
     if (halted) break;
   }
   return AQP_OK;
@@ -1369,6 +1574,7 @@ static int run_eager(aqp_solver *s, int64_t n_iters) {
 
 int aqp_solver_run(aqp_solver *s, int64_t n_iters) {
   if (!s) return fail(AQP_EINVAL, "NULL argument");
+  if (!s->exec && !s->eager) return fail(AQP_ESTATE, "sharded solver is not connected (aqp_solver_connect)");
   if (n_iters <= 0) return AQP_OK;
   // host mirror is current (the host only changes scalars between windows)
   s->h.s.iters_done = 0;
@@ -1388,9 +1594,14 @@ int aqp_solver_check(aqp_solver *s, int with_rays, aqp_check_result *out) {
   GridRed gr = s->gr;
   const int rays = with_rays ? 1 : 0;
   AQP_CUDA(cudaMemsetAsync(&s->d_ctrl->red[0], 0, sizeof(double) * R_PW, st));
-  { OpChkX o{}; o.v = v; o.rays = rays; AQP_CUDA(run_elem(st, p->n, o, gr)); }
-  { OpChkY o{}; o.v = v; o.rays = rays; AQP_CUDA(run_elem(st, p->m, o, gr)); }
+  { OpChkX o{}; o.v = v; o.rays = rays; AQP_CUDA(run_elem(st, v.nl, o, gr)); }
+  AQP_TRY(push_buf(s, PB_XEVAL));
+  { OpChkY o{}; o.v = v; o.rays = rays; AQP_CUDA(run_elem(st, v.ml, o, gr)); }
   { OpChkA o{}; o.v = v; o.rays = rays; AQP_CUDA(run_spmv(st, p->A, o, gr)); }
+  if (rays) {  // normalised y-ray candidates: gathered by the A' ray passes
+    AQP_TRY(push_buf(s, PB_DY0));
+    AQP_TRY(push_buf(s, PB_DY1));
+  }
   if (p->quad_kind != AQP_QUAD_DIAGONAL) {
     if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
       OpRx rx{}; rx.v = v; rx.src = 2;
@@ -1402,8 +1613,10 @@ int aqp_solver_check(aqp_solver *s, int with_rays, aqp_check_result *out) {
     AQP_CUDA(run_spmv(st, p->Q, q, gr));
   }
   { OpStoreT<false> a{}; a.v = v; a.src = 1; a.dst = 1; a.red = -1; AQP_CUDA(run_spmv(st, p->At, a, gr)); }
-  { OpChkR o{}; o.v = v; o.rays = rays; AQP_CUDA(run_elem(st, p->n, o, gr)); }
+  { OpChkR o{}; o.v = v; o.rays = rays; AQP_CUDA(run_elem(st, v.nl, o, gr)); }
   if (rays) {
+    AQP_TRY(push_buf(s, PB_DX0));
+    AQP_TRY(push_buf(s, PB_DX1));
     for (int j = 0; j < 2; ++j) {
       OpChkYRay o{}; o.v = v; o.j = j;
       AQP_CUDA(run_spmv(st, p->At, o, gr));
@@ -1413,7 +1626,7 @@ int aqp_solver_check(aqp_solver *s, int with_rays, aqp_check_result *out) {
       AQP_CUDA(run_spmv(st, p->A, a, gr));
       if (p->quad_kind == AQP_QUAD_DIAGONAL) {
         OpChkXRayT<false> q{}; q.v = v; q.j = j; q.which = 1;
-        AQP_CUDA(run_elem(st, p->n, q, gr));
+        AQP_CUDA(run_elem(st, v.nl, q, gr));
       } else {
         if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
           OpXRayRx rx{}; rx.v = v; rx.src = 3 + j; rx.j = j;
@@ -1490,9 +1703,22 @@ int aqp_solver_read(aqp_solver *s, int which, double *host_out, int64_t len) {
     AQP_TRY(pull_ctrl(s));
     src = which == 1 ? pick3(v.ys, s->h.ycur) : pick3(v.xs, s->h.xcur);
   }
+  const bool yside = which == 1 || which == 3 || which == 4;
+  if (s->shard) {
+    // collective: every rank replicates its slice, then reads the full vector
+    static const int kPush[8] = {PB_XEVAL, PB_Y, PB_RS, PB_DY0, PB_DY1, PB_DX0, PB_DX1, PB_X};
+    AQP_TRY(push_buf(s, kPush[which]));
+  }
+  src -= yside ? v.yoff : v.xoff;
   cudaStream_t st = s->p->ctx->stream;
-  if (need) AQP_CUDA(cudaMemcpyAsync(host_out, src, need * 8, cudaMemcpyDeviceToHost, st));
+  for (int64_t off = 0; off < need; off += (int64_t)aqp_solver::kBounce) {  // via the pinned bounce buffer
+    const int64_t len = std::min<int64_t>(need - off, (int64_t)aqp_solver::kBounce);
+    AQP_CUDA(cudaMemcpyAsync(s->bounce, src + off, len * 8, cudaMemcpyDeviceToHost, st));
+    AQP_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(host_out + off, s->bounce, len * 8);
+  }
   AQP_CUDA(cudaStreamSynchronize(st));
+  if (s->shard) AQP_TRY(pull_ctrl(s));  // surfaces an exchange timeout
   return AQP_OK;
 }
 
@@ -1511,13 +1737,20 @@ int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, do
   cudaStream_t st = p->ctx->stream;
   const SV &v = s->v;
   GridRed gr = s->gr;
-  const int64_t n = p->n;
+  const int64_t n = v.nl;
   *annihilated = 0;
   AQP_TRY(poke(s, &Ctrl::pw_stop, 0));
-  AQP_CUDA(cudaMemcpyAsync(pick3(v.xbb, 0), host_v0, n * 8, cudaMemcpyHostToDevice, st));
+  // every rank holds the whole start vector (drawn on the host): copy it whole
+  for (int64_t off = 0; off < p->n; off += (int64_t)aqp_solver::kBounce) {
+    const int64_t len = std::min<int64_t>(p->n - off, (int64_t)aqp_solver::kBounce);
+    AQP_CUDA(cudaStreamSynchronize(st));  // the bounce buffer is free again
+    std::memcpy(s->bounce, host_v0 + off, len * 8);
+    AQP_CUDA(cudaMemcpyAsync(pick3(v.xbb, 0) - v.xoff + off, s->bounce, len * 8, cudaMemcpyHostToDevice, st));
+  }
   // nv = |v|; u = v / nv; |A u| > 0 ?
   { OpPwNorm o{}; o.v = v; o.idx = 0; o.slot = R_PW; AQP_CUDA(run_elem(st, n, o, gr)); }
   { OpPwScale o{}; o.v = v; o.src = 0; o.dst = 1; o.slot = R_PW; AQP_CUDA(run_elem(st, n, o, gr)); }
+  AQP_TRY(push_buf(s, PB_PW));
   { OpStoreT<false> a{}; a.v = v; a.src = 2; a.dst = 2; a.red = R_PW + 1; AQP_CUDA(run_spmv(st, p->A, a, gr)); }
   AQP_TRY(pull_ctrl(s));
   if (!(s->h.red[R_PW] > 0.0) || !(s->h.red[R_PW + 1] > 0.0)) {
@@ -1527,12 +1760,14 @@ int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, do
   for (int it = 0; it < iters; ++it) {
     OpStoreT<false> a{}; a.v = v; a.src = 2; a.dst = 2; a.red = -1;           // t = A v
     AQP_CUDA(run_spmv(st, p->A, a, gr));
+    AQP_TRY(push_buf(s, PB_TM));
     OpStoreT<false> b{}; b.v = v; b.src = 3; b.dst = 3; b.red = R_PW + 2;     // w = A't, |w|^2
     AQP_CUDA(run_spmv(st, p->At, b, gr));
     k_pw_check<<<1, 1, 0, st>>>(s->d_ctrl, R_PW + 2);
     AQP_CUDA(cudaGetLastError());
     OpPwScale c{}; c.v = v; c.src = 2; c.dst = 1; c.slot = R_PW + 2;          // v = w / |w|
     AQP_CUDA(run_elem(st, n, c, gr));
+    AQP_TRY(push_buf(s, PB_PW));
   }
   // final |A v| (the stop flag must not suppress it)
   AQP_TRY(poke(s, &Ctrl::pw_stop, 0));
@@ -1603,7 +1838,7 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
       case 1: {
         OpStep o{};
         o.v = v;
-        AQP_CUDA(run_elem(st, p->n, o, gr));
+        AQP_CUDA(run_elem(st, v.nl, o, gr));
         break;
       }
       case 2: {
@@ -1621,7 +1856,7 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
       case 4: {
         OpXPost o{};
         o.v = v;
-        AQP_CUDA(run_elem_fin(st, p->n, o, gr));
+        AQP_CUDA(run_elem_fin(st, v.nl, o, gr));
         break;
       }
       default: return fail(AQP_EINVAL, "unknown kernel id");
@@ -1635,6 +1870,46 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   *avg_ms = total / reps;
+  return AQP_OK;
+}
+
+// ---------------------------------------------------------------- CUDA IPC (peer workspaces)
+typedef int (*PFN_addr_range)(unsigned long long *, size_t *, unsigned long long);
+
+int aqp_ipc_get_handle(const void *dev_ptr, void *handle64, size_t *offset) {
+  if (!dev_ptr || !handle64 || !offset) return fail(AQP_EINVAL, "NULL argument");
+  static PFN_addr_range fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *f = nullptr;
+    AQP_CUDA(cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &f, 12000, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f) return fail(AQP_ECUDA, "cuMemGetAddressRange unavailable");
+    fn = (PFN_addr_range)f;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0) return fail(AQP_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  AQP_CUDA(cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle64, &h, sizeof(h));
+  *offset = (size_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+  return AQP_OK;
+}
+
+int aqp_ipc_open(const void *handle64, size_t offset, void **dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail(AQP_EINVAL, "NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  void *base = nullptr;
+  AQP_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr = (char *)base + offset;
+  return AQP_OK;
+}
+
+int aqp_ipc_close(void *dev_ptr, size_t offset) {
+  if (!dev_ptr) return fail(AQP_EINVAL, "NULL argument");
+  AQP_CUDA(cudaIpcCloseMemHandle((char *)dev_ptr - offset));
   return AQP_OK;
 }
 

@@ -120,6 +120,17 @@ class DeviceProblem:
         nat.check(lib.aqp_problem_get_info(h, C.byref(info)))
         self.info = info
 
+    def shard(self, rank: int, nranks: int, n0: int, n1: int, m0: int, m1: int):
+        """Restrict this rank's passes to rows [n0,n1) of A'/Q and [m0,m1) of A
+        (aqp_problem_shard)."""
+        sh = nat.Shard(rank=rank, nranks=nranks, n0=n0, n1=n1, m0=m0, m1=m1)
+        nat.check(self.ctx.lib.aqp_problem_shard(self.handle, C.byref(sh)), "aqp_problem_shard")
+        info = nat.ProblemInfo()
+        nat.check(self.ctx.lib.aqp_problem_get_info(self.handle, C.byref(info)))
+        self.info = info
+        self.rank, self.nranks = rank, nranks
+        self.rows = (n0, n1, m0, m1)
+
     def close(self):
         if getattr(self, "handle", None):
             self.ctx.lib.aqp_problem_destroy(self.handle)
@@ -226,6 +237,18 @@ class DeviceSolver:
         buf = (C.c_int64 * 3)()
         nat.check(self.lib.aqp_solver_counters(self.handle, buf))
         return bool(buf[2])
+
+    # -- row shards -------------------------------------------------------------
+    def exchange_region(self):
+        """(device address, bytes) of the peer-written front of the workspace."""
+        base, nbytes = C.c_void_p(), C.c_size_t()
+        nat.check(self.lib.aqp_solver_exchange_region(self.handle, C.byref(base), C.byref(nbytes)))
+        return int(base.value), int(nbytes.value)
+
+    def connect(self, peer_bases):
+        """Bind the peers' workspace mappings (index = rank) and build the graph."""
+        arr = (C.c_void_p * len(peer_bases))(*[C.c_void_p(int(b)) for b in peer_bases])
+        nat.check(self.lib.aqp_solver_connect(self.handle, arr, len(peer_bases)), "aqp_solver_connect")
 
     def close(self):
         if getattr(self, "handle", None):

@@ -189,12 +189,16 @@ def estimate_eta(solver: DeviceSolver, problem: QpProblem, params: SolverParams)
 class _Run:
     """One solve: device objects + the reference's loop locals."""
 
-    def __init__(self, problem: QpProblem, params: SolverParams, progress, device: int):
+    def __init__(self, problem: QpProblem, params: SolverParams, progress, device: int, group=None):
         self.problem = problem
         self.params = params
         self.progress = progress
         ctx = DeviceContext.get(device)
         self.dev = DeviceProblem(problem, ctx)
+        if group is not None:  # row shard of a multi-GPU solve (shard.py)
+            from .shard import rows_of
+
+            self.dev.shard(group.rank, group.nranks, *rows_of(problem, group))
         gamma = params.gamma_sys if params.gamma_sys is not None else certify.default_gamma_sys(problem)
         self.gamma_sys = gamma
         self.con_scale = certify.finite_bound_scale(problem.con_bounds)
@@ -204,6 +208,8 @@ class _Run:
             self.dev, eps_tol=params.eps_tol, eps_inf=params.eps_inf, gamma_sys=gamma,
             tol_scale=ip.scale, tol_floor=ip.floor, diag_bound=problem.quad.diag_bound(),
             adaptive=ip.adaptive, max_inner=ip.max_inner, halpern=params.halpern)
+        if group is not None:
+            group.connect(self.solver)
 
     def report(self, cr, need_slack: bool) -> ResidualReport:
         slack = self.solver.read(DeviceSolver.DUAL_SLACK) if need_slack else None
@@ -211,7 +217,7 @@ class _Run:
 
 
 def solve(problem, params: Optional[SolverParams] = None, progress: Optional[ProgressCallback] = None,
-          device: int = 0, monitor: Optional[Callable[[int, int], None]] = None) -> SolveResult:
+          device: int = 0, monitor: Optional[Callable[[int, int], None]] = None, group=None) -> SolveResult:
     """Run until optimality, an infeasibility certificate, or a limit
     (engine.py:339-498).  ``problem`` may be this package's QpProblem or the
     reference's (rebuilt field by field).
@@ -219,12 +225,16 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
     ``monitor(outer, inner)`` (extension, not in the reference API) is called
     at every certification point right after the device check, with the
     cumulative outer and BB-inner iteration counts -- bench.py brackets
-    certification windows with CUDA events from it."""
+    certification windows with CUDA events from it.
+
+    ``group`` (extension, shard.PeerGroup): solve this problem row-sharded
+    with the group's other ranks; every rank calls solve
+    with the same problem and params and gets the same result."""
     params = params or SolverParams()
     problem = QpProblem.from_any(problem)
     validate(problem)
     start = time.monotonic()
-    run = _Run(problem, params, progress, device)
+    run = _Run(problem, params, progress, device, group)
     sol = run.solver
     rs = _Round(omega=params.omega0, eta=0.0, theta=params.theta)
     rs.eta = estimate_eta(sol, problem, params)
@@ -244,8 +254,10 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
                            outer_iterations=n_outer, inner_iterations=n_inner, restarts=restarts,
                            seconds=time.monotonic() - start)
 
+    # sharded: reading the slack is collective, so every rank reads it
+    want_slack = progress is not None or group is not None
     cr = sol.check(with_rays=False)
-    report = run.report(cr, progress is not None)
+    report = run.report(cr, want_slack)
     rs.best_residual_round_start = report.kkt_max
     rs.last_check_kkt = report.kkt_max
     if progress is not None:
@@ -312,7 +324,7 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
         cr = sol.check(with_rays=True)
         if monitor is not None:
             monitor(n_outer, n_inner)
-        report = run.report(cr, progress is not None)
+        report = run.report(cr, want_slack)
         kkt = report.kkt_max
         if progress is not None:
             progress(n_outer, report, rs.omega, rs.round)
@@ -358,8 +370,12 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
             push(k=0, omega=rs.omega)
         else:
             rs.last_check_kkt = kkt
-        if params.time_limit is not None and time.monotonic() - start >= params.time_limit:
-            return finish(SolveStatus.TIME_LIMIT, report, None)
+        if params.time_limit is not None:
+            out_of_time = time.monotonic() - start >= params.time_limit
+            if group is not None:  # a clock reading: every rank must take the same branch
+                out_of_time = group.agree_any(out_of_time)
+            if out_of_time:
+                return finish(SolveStatus.TIME_LIMIT, report, None)
 
     cr = sol.check(with_rays=False)
     return finish(SolveStatus.ITERATION_LIMIT, run.report(cr, False), None)
