@@ -24,9 +24,14 @@ configs[1] -- solved to 1e-8 relative KKT through the public
 * ``cpu_baseline``: the reference solver (oracle/_ref, Cython) on the host,
   1 core, bounded sample of the same solve (rank 0, N = 1).
 
-N > 1 (torchrun): replicas -- each rank solves its own C2 instance (seed =
-rank); weak scaling.  ``--impl reference`` times the reference CPU solver
-(rank 0 only) on the same workload and metric.
+N > 1 (torchrun): ONE C2 solve row-sharded over the N GPUs (SURVEY.md §8(e),
+paper_2602_23967_b200/shard.py): rank r owns a block of rows of A, A' and Q,
+the gathered vectors are replicated by NVLink peer stores and every
+reduction is a one-block mailbox exchange -- strong scaling of the same
+workload; ``value`` is that solve's BB iterations / s (max-over-ranks device
+time).  ``--replicas`` instead runs N independent C2 solves (weak scaling).
+``--impl reference`` times the reference CPU solver (rank 0 only) on the
+same workload and metric.
 """
 
 from __future__ import annotations
@@ -171,8 +176,14 @@ def run_ours(args, world, rank, local):
     from paper_2602_23967_b200 import _native as nat
 
     torch.cuda.set_device(local)
-    seed = rank
+    sharded = world > 1 and not args.replicas
+    seed = 0 if sharded else rank
     problem = generators.lasso_style_qp(SPEC_N, SPEC_M, seed=seed)
+    group = None
+    if sharded:
+        from paper_2602_23967_b200.shard import DistGroup
+
+        group = DistGroup()
     n, m = problem.n, problem.m
     stream = torch.cuda.current_stream()
     marks = {}
@@ -192,7 +203,7 @@ def run_ours(args, world, rank, local):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = aq.solve(problem, aq.SolverParams(eps_tol=EPS), device=local, monitor=monitor)
+    res = aq.solve(problem, aq.SolverParams(eps_tol=EPS), device=local, monitor=monitor, group=group)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     clk = clocks.stop()
@@ -209,6 +220,8 @@ def run_ours(args, world, rank, local):
         sm = t.clone()
         torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
         ms_max, inner_sum, inner_total_sum, wall_max = mx[0].item(), sm[1].item(), sm[2].item(), mx[3].item()
+        if sharded:  # one solve: every rank reports the same counts
+            inner_sum, inner_total_sum = inner, res.inner_iterations
     else:
         ms_max, inner_sum, inner_total_sum, wall_max = ms, inner, res.inner_iterations, wall
     value = inner_sum / (ms_max / 1e3)
@@ -253,12 +266,14 @@ def run_ours(args, world, rank, local):
         return
     line = {
         "metric": METRIC, "value": value, "unit": "inner_iters/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_max / K if K else None, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_max / K if K else None, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"C2 lasso-style QP n={n} m={m} nnz(A)={problem.constraint_matrix.nnz} "
                                f"nnz(Q_full)={nnz_q} (BASELINE configs[1])",
                    "step": f"one certification window = {CHECK_EVERY} outer iterations + device check",
-                   "eps_tol": EPS, "parallelism": "replicas" if world > 1 else "single",
+                   "eps_tol": EPS,
+                   "parallelism": f"rowshard{world}" if sharded else ("replicas" if world > 1 else "single"),
                    "l2": "inputs (~230 MB of matrices+vectors per iteration) exceed the 126 MB L2; "
                          "roofline kernel timed with a 512 MB L2 flush before every launch"},
         "solve": {"status": res.status.value, "outer": res.outer_iterations, "inner": res.inner_iterations,
@@ -295,6 +310,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent solves instead of one sharded solve")
     args = ap.parse_args()
     world, rank, local = dist_init()
     if args.impl == "reference":

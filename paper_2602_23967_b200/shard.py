@@ -199,7 +199,12 @@ class LocalGroup(PeerGroup):
 def solve_local(problem, params=None, nranks: int = 2, device: int = 0, timeout: float = 3600.0, **kw):
     """Row-sharded solve over `nranks` virtual ranks on one device (threads,
     one CUDA stream each).  Returns the per-rank SolveResults (identical
-    status / counts / vectors on every rank)."""
+    status / counts / vectors on every rank).
+
+    The ranks' exchange kernels spin on each other, so their streams must sit
+    on distinct hardware queues: run with CUDA_DEVICE_MAX_CONNECTIONS=32 set
+    before CUDA initialises (tests/conftest.py does).  A violated assumption
+    surfaces as an exchange-timeout DeviceError, never as a hang."""
     import torch
 
     from .engine import solve

@@ -5,6 +5,12 @@ import json
 import os
 import sys
 
+# Row-shard tests run several virtual ranks (one CUDA stream each) on the one
+# GPU of the test box; their spinning exchanges need every rank's stream on
+# its own hardware queue (no head-of-line blocking behind another rank), so
+# ask for the maximum number of queues before CUDA is initialised.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 import pytest
 

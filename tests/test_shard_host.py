@@ -1,0 +1,105 @@
+"""CPU: host side of the row-sharded path -- the row
+partition, the host-level agreement of LocalGroup (threads) and DistGroup
+(torch.distributed gloo, world size 2).  The device exchange itself is
+covered by tests/test_gpu_shard.py."""
+
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import instances
+from paper_2602_23967_b200 import shard
+
+
+def _check_partition(parts, n, m):
+    assert parts[0][0] == 0 and parts[-1][1] == n and parts[0][2] == 0 and parts[-1][3] == m
+    for (a0, a1, b0, b1), (c0, c1, d0, d1) in zip(parts, parts[1:]):
+        assert a1 == c0 and b1 == d0
+    for n0, n1, m0, m1 in parts:
+        assert n1 > n0 and m1 > m0
+
+
+@pytest.mark.parametrize("spec", ["c1:0", "rqp:500:300:diagonal:0.02:5", "c5:5e3:50:0"])
+@pytest.mark.parametrize("nranks", [1, 2, 3, 8])
+def test_partition_covers_rows_contiguously(spec, nranks):
+    p = instances.build(spec)
+    parts = shard.partition(p, nranks)
+    assert len(parts) == nranks
+    _check_partition(parts, p.n, p.m)
+
+
+def test_partition_balances_bytes():
+    p = instances.build("c1:0")
+    parts = shard.partition(p, 4)
+    a = p.constraint_matrix
+    wy = 64.0 + 12.0 * np.diff(a.indptr)
+    loads = [wy[m0:m1].sum() for _, _, m0, m1 in parts]
+    assert max(loads) <= 1.15 * (sum(loads) / 4)
+
+
+def test_partition_edge_cases():
+    assert shard._split(np.ones(8), 8) == list(range(9))
+    # all the weight in one row still leaves every rank a row
+    w = np.zeros(10)
+    w[0] = 1e9
+    cuts = shard._split(w, 4)
+    assert cuts[0] == 0 and cuts[-1] == 10 and all(b > a for a, b in zip(cuts, cuts[1:]))
+    with pytest.raises(ValueError):
+        shard._split(np.ones(3), 4)
+    with pytest.raises(ValueError):
+        shard.partition(instances.build("c1:0"), 9)
+
+
+def test_local_group_agree_any():
+    groups = shard.LocalGroup.create(3)
+    out = [None] * 3
+
+    def work(r):
+        out[r] = [groups[r].agree_any(r == 2 and k == 1) for k in range(3)]
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(30)
+    assert out == [[False, True, False]] * 3
+
+
+def _dist_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = shard.DistGroup()
+        agreed = [g.agree_any(rank == 1 and k == 0) for k in range(2)]
+        p = instances.build("c1:1")
+        rows = shard.rows_of(p, g)
+        q.put((rank, agreed, rows))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dist_group_gloo_world2():
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for pr in procs:
+        pr.join(60)
+        assert pr.exitcode == 0
+    (r0, a0, rows0), (r1, a1, rows1) = res
+    assert a0 == a1 == [True, False]
+    p = instances.build("c1:1")
+    assert [rows0, rows1] == shard.partition(p, 2)
