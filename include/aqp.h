@@ -121,6 +121,13 @@ typedef struct {
   const int64_t *r_indices;
   const double *r_data;
   int64_t r_nnz;
+  /* LOW_RANK: every row of R is full (indptr = i*n, indices = 0..n-1), so
+   * r_data IS R dense row-major (r_rows x n); r_indices is not read.  The
+   * factor-model case (linalg.py:230-266 with R = F'): held dense on the
+   * device, R x and R'v become streaming passes (16 B per entry per apply
+   * instead of 24 B of CSR for R plus R'). */
+  int32_t r_dense;
+  int32_t pad0_;
   /* vectors */
   const double *cost;   /* n */
   const double *var_lo; /* n */
@@ -263,7 +270,8 @@ int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, do
                              int *annihilated);
 /* Stand-alone event timing of one hot kernel (bench.py roofline): kernel
  * 0 = BB gradient SpMV pass, 1 = BB step, 2 = P1, 3 = P2 (+fold), 4 = X
- * (+fold), 5 = fold/finalize of pass 0; each of `reps`
+ * (+fold), 5 = fold/finalize of pass 0, 6 = dense R x (+ its fold), 7 = dense
+ * R'(R x) (dense low-rank problems only); each of `reps`
  * launches follows an L2 flush (streaming read of flush_bytes at flush).  Average
  * device milliseconds per launch in *avg_ms.  Clobbers BB scratch. */
 int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, size_t flush_bytes, double *avg_ms);

@@ -37,6 +37,7 @@ class ProblemDesc(C.Structure):
         ("q_diag", C.c_void_p),
         ("r_rows", C.c_int64),
         ("r_indptr", C.c_void_p), ("r_indices", C.c_void_p), ("r_data", C.c_void_p), ("r_nnz", C.c_int64),
+        ("r_dense", C.c_int32), ("pad0_", C.c_int32),
         ("cost", C.c_void_p), ("var_lo", C.c_void_p), ("var_hi", C.c_void_p),
         ("con_lo", C.c_void_p), ("con_hi", C.c_void_p),
     ]

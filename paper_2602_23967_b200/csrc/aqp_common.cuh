@@ -181,15 +181,27 @@ struct Comm {
   long long delta[kMaxRanks] = {};  // byte offset local -> rank k's mapping of the same buffer
 };
 
+// c.delta[k] for a run-time k without indexing the kernel-parameter array
+// dynamically (that would copy the whole op into local memory)
+__device__ __forceinline__ long long peer_delta(const Comm &c, int k) {
+  long long d = 0;
+#pragma unroll
+  for (int j = 0; j < kMaxRanks; ++j)
+    if (j == k) d = c.delta[j];
+  return d;
+}
 template <class T>
 __device__ __forceinline__ T *peer_addr(const Comm &c, T *p, int k) {
-  return reinterpret_cast<T *>(reinterpret_cast<char *>(p) + c.delta[k]);
+  return reinterpret_cast<T *>(reinterpret_cast<char *>(p) + peer_delta(c, k));
 }
 
 // store `val` at p[i] on every peer (the local store is the caller's)
 __device__ __forceinline__ void peer_put(const Comm &c, double *p, int64_t i, double val) {
-  for (int k = 0; k < c.nranks; ++k)
-    if (k != c.rank) peer_addr(c, p, k)[i] = val;
+  if (c.nranks <= 1) return;
+#pragma unroll
+  for (int k = 0; k < kMaxRanks; ++k)
+    if (k < c.nranks && k != c.rank)
+      *reinterpret_cast<double *>(reinterpret_cast<char *>(p + i) + c.delta[k]) = val;
 }
 
 __device__ __forceinline__ unsigned long long global_ns_() {

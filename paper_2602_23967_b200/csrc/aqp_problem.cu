@@ -460,8 +460,12 @@ static void layout_problem(Bump &b, const aqp_problem_desc *d, aqp_problem *p) {
   layout_csr(b, p->sAt, n, d->a_nnz);
   if (d->quad_kind != AQP_QUAD_DIAGONAL) layout_csr(b, p->sQ, n, 2 * d->q_nnz);
   if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
-    layout_csr(b, p->sR, d->r_rows, d->r_nnz);
-    layout_csr(b, p->sRt, n, d->r_nnz);
+    if (d->r_dense) {
+      p->sR.val = (double *)b.take(std::max<int64_t>(d->r_rows * n, 1) * 8);
+    } else {
+      layout_csr(b, p->sR, d->r_rows, d->r_nnz);
+      layout_csr(b, p->sRt, n, d->r_nnz);
+    }
   }
   p->c = (double *)b.take(std::max<int64_t>(n, 1) * 8);
   p->vlo = (double *)b.take(std::max<int64_t>(n, 1) * 8);
@@ -487,7 +491,8 @@ int aqp_problem_sizes(const aqp_problem_desc *d, size_t *persistent_bytes, size_
     const size_t up = (size_t)(d->n + 1) * 4 + (size_t)std::max<int64_t>(d->q_nnz, 1) * 12 + 1024;
     sc = std::max(sc, up + symmetrize_scratch_bytes(d->q_nnz, d->n));
   }
-  if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) sc = std::max(sc, transpose_scratch_bytes(d->r_nnz, d->n));
+  if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && !d->r_dense)
+    sc = std::max(sc, transpose_scratch_bytes(d->r_nnz, d->n));
   if (persistent_bytes) *persistent_bytes = b.used + 256;
   if (scratch_bytes) *scratch_bytes = sc;
   return AQP_OK;
@@ -564,7 +569,18 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
     rc = symmetrize_csr(ctx, U, p->sQ, p->Q, false, rest, &p->q_full_nnz);
     if (rc) return cleanup(rc);
     if (n) AQP_CUDA(cudaMemcpyAsync(p->qd, d->q_diag, n * 8, cudaMemcpyDeviceToDevice, st));
-    if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
+    if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && d->r_dense) {
+      // full rows: the CSR values are R row-major; check the implied pattern
+      for (int64_t i = 0; i <= d->r_rows; ++i)
+        if (host_r_indptr[i] != i * n) return cleanup(fail(AQP_EINVAL, "r_dense set but R rows are not full"));
+      if (d->r_nnz != d->r_rows * n) return cleanup(fail(AQP_EINVAL, "r_dense: r_nnz != r_rows * n"));
+      if (d->r_nnz) AQP_CUDA(cudaMemcpyAsync(p->sR.val, d->r_data, d->r_nnz * 8, cudaMemcpyDeviceToDevice, st));
+      p->R.rows = (int)d->r_rows;
+      p->R.cols = (int)n;
+      p->R.nnz = d->r_nnz;
+      p->R.val = p->sR.val;
+      p->r_dense = 1;
+    } else if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
       rc = upload_csr(ctx, p->sR, p->R, d->r_rows, d->n, d->r_indptr, d->r_indices, d->r_data, d->r_nnz,
                       host_r_indptr, false, p->bad);
       if (!rc) rc = transpose_csr(ctx, p->R, p->sRt, p->Rt, false, sc);
@@ -592,6 +608,7 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
   p->info.at_nnz = p->At.nnz;
   p->info.q_full_nnz = p->q_full_nnz;
   p->info.r_rows = d->r_rows;
+  p->info.r_dense = p->r_dense;
   p->info.quad_kind = d->quad_kind;
   p->info.a_items = p->A.nitems;
   p->info.at_items = p->At.nitems;

@@ -68,6 +68,9 @@ struct SV {
   double *xlast, *ylast, *xblk, *yblk, *xavgp, *yavgp;
   double *lin, *xbar, *xbb[3], *gbb[2];
   double *rx, *rtv;        // low-rank temporaries (k and n)
+  const double *Rd;        // dense R (k x n row-major) when the problem holds R dense
+  double *rxpart;          // dense R x: per-block partials [k][blocks]
+  int rk;                  // rows of R
   double *xeval, *qx, *aty, *rs, *dx[2], *dy[2];
   double *tm;              // m-length temporary (power iteration)
   Ctrl *ctrl;
@@ -494,6 +497,101 @@ struct OpRtv {
   __device__ void row(int r, double s, RedVals<0, 0> &) const { v.rtv[r] = s; }
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
+
+// ---------------------------------------------------------------- dense low-rank factor
+// Factor-model Q = P + R'R with R dense (k x n row-major, aqp_problem_desc.r_dense):
+// R x is k streaming dot products over n (each block folds a column chunk of
+// every row into per-block partials, a k-block kernel folds those in block
+// order), R'(Rx) is a streaming pass whose entry i sums k products in row
+// order -- bitwise the order of the reference's csr_matvec_t over R
+// (_core.pyx:45-59).  Both read R once: 8 k n bytes per pass.
+constexpr int kRxCols = 4096;  // columns per block of the R x pass (32 KB of x in smem)
+inline int64_t dense_rx_blocks(int64_t n) { return std::max<int64_t>((n + kRxCols - 1) / kRxCols, 1); }
+__device__ __forceinline__ bool cand_valid(const Ctrl *ct, int j, double norm);
+
+__device__ __forceinline__ const double *lowrank_src(const SV &v, int src) {
+  const Ctrl *ct = v.ctrl;
+  return src == 0 ? pick3(v.xbb, 0) : src == 1 ? pick3(v.xbb, ct->bb_new) : src == 2 ? v.xeval : pick2(v.dx, src - 3);
+}
+// x-ray candidates only when the cheap test passed (certify.py:148-157)
+__device__ __forceinline__ bool lowrank_skip(const SV &v, int src) {
+  if (src < 3) return false;
+  const Ctrl *ct = v.ctrl;
+  const int j = src - 3;
+  const double *xr = ct->red + R_XR + 5 * j;
+  return !(cand_valid(ct, j, xr[0]) && xr[1] < -v.eps_tol);
+}
+
+__global__ void __launch_bounds__(kThreads) k_dense_rx(SV v, int src) {
+  __shared__ __align__(16) double xs[kRxCols];
+  pdl_wait();
+  if (lowrank_skip(v, src)) return;
+  const double *x = lowrank_src(v, src);
+  const int64_t n = v.n;
+  const int64_t j0 = (int64_t)blockIdx.x * kRxCols;
+  const int len = (int)min((int64_t)kRxCols, n - j0);
+  for (int t = threadIdx.x; t < len; t += kThreads) xs[t] = x[j0 + t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec = (n & 1) == 0;  // rows 16-byte aligned
+  for (int kk = warp; kk < v.rk; kk += kWarps) {
+    const double *row = v.Rd + (int64_t)kk * n + j0;
+    double a0 = 0.0, a1 = 0.0;
+    if (vec) {
+      const double2 *r2 = reinterpret_cast<const double2 *>(row);
+      const double2 *x2 = reinterpret_cast<const double2 *>(xs);
+      const int h = len >> 1;
+#pragma unroll 4
+      for (int u = lane; u < h; u += 32) {
+        const double2 r = __ldcs(r2 + u);  // streamed once per pass: do not keep in L2
+        const double2 q = x2[u];
+        a0 += r.x * q.x;
+        a1 += r.y * q.y;
+      }
+      if ((len & 1) && lane == 0) a0 += row[len - 1] * xs[len - 1];
+    } else {
+#pragma unroll 4
+      for (int u = lane; u < len; u += 32) a0 += __ldcs(row + u) * xs[u];
+    }
+    double a = a0 + a1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+    if (lane == 0) v.rxpart[(size_t)kk * gridDim.x + blockIdx.x] = a;
+  }
+  pdl_trigger();
+}
+
+// rx[k] = fold of the k-th row's block partials (block order, fixed tree)
+__global__ void __launch_bounds__(kThreads) k_dense_rx_fold(SV v, int src, int nb) {
+  __shared__ double sred[kWarps * kMaxRed];
+  pdl_wait();
+  pdl_trigger();
+  if (lowrank_skip(v, src)) return;
+  const int kk = blockIdx.x;
+  RedVals<1, 0> a;
+  a.zero();
+  for (int b = threadIdx.x; b < nb; b += kThreads) a.s[0] += v.rxpart[(size_t)kk * nb + b];
+  block_reduce<1, 0>(a, sred);
+  if (threadIdx.x == 0) v.rx[kk] = a.s[0];
+}
+
+// rtv[i] = sum_k R[k, i] rx[k], k ascending
+__global__ void __launch_bounds__(kThreads) k_dense_rtv(SV v, int src) {
+  __shared__ double rxs[1024];
+  pdl_wait();
+  if (lowrank_skip(v, src)) return;
+  const int k = v.rk;
+  for (int t = threadIdx.x; t < k && t < 1024; t += kThreads) rxs[t] = v.rx[t];
+  __syncthreads();
+  const int64_t n = v.n;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    double s = 0.0;
+#pragma unroll 8
+    for (int kk = 0; kk < k; ++kk) s += __ldcs(v.Rd + (int64_t)kk * n + i) * (kk < 1024 ? rxs[kk] : v.rx[kk]);
+    v.rtv[i] = s;
+  }
+  pdl_trigger();
+}
 
 // ================================================================ certification ops
 __device__ __forceinline__ bool cand_valid(const Ctrl *ct, int j, double norm) {
@@ -1017,6 +1115,7 @@ void layout_solver(Bump &b, aqp_problem *p, SV &v, Ctrl **ctrl, GridRed &gr) {
   for (const DevCsr *M : {&p->A, &p->At, &p->Q, &p->R, &p->Rt}) maxg = std::max<int64_t>(maxg, M->nitems);
   gr.partials = (double *)b.take(maxg * kMaxRed * 8);
   gr.ticket = (unsigned *)b.take(64);
+  if (p->r_dense) v.rxpart = (double *)b.take(std::max<int64_t>(p->R.rows, 1) * dense_rx_blocks(p->n) * 8);
 }
 
 // explicit graph construction helpers
@@ -1128,8 +1227,29 @@ cudaError_t run_elem_fin(cudaStream_t st, int64_t n, const Op &op, GridRed gr) {
   return cudaGetLastError();
 }
 
+// stream launch of the dense R x / R'(R x) passes (eager windows, checks)
+int dense_lowrank(aqp_solver *s, int src) {
+  aqp_problem *p = s->p;
+  cudaStream_t st = p->ctx->stream;
+  const int nb = (int)dense_rx_blocks(p->n);
+  k_dense_rx<<<nb, kThreads, 0, st>>>(s->v, src);
+  k_dense_rx_fold<<<p->R.rows, kThreads, 0, st>>>(s->v, src, nb);
+  k_dense_rtv<<<elem_grid(p->n), kThreads, 0, st>>>(s->v, src);
+  AQP_CUDA(cudaGetLastError());
+  return AQP_OK;
+}
+
 int add_lowrank(aqp_solver *s, cudaGraph_t g, GNode &last, int src) {
   aqp_problem *p = s->p;
+  if (p->r_dense) {
+    SV v = s->v;
+    v.in_graph = 1;
+    const int nb = (int)dense_rx_blocks(p->n);
+    AQP_CUDA(add_node(g, last, (unsigned)nb, k_dense_rx, v, src));
+    AQP_CUDA(add_node(g, last, (unsigned)p->R.rows, k_dense_rx_fold, v, src, nb));
+    AQP_CUDA(add_node(g, last, (unsigned)elem_grid(p->n), k_dense_rtv, v, src));
+    return AQP_OK;
+  }
   OpRx rx{};
   rx.v = s->v;
   rx.v.in_graph = 1;
@@ -1187,7 +1307,7 @@ int build_graph(aqp_solver *s) {
     OpGrad<true> g0{};
     g0.v = v;
     AQP_CUDA(node_spmv_fin(body, last, p->Q, g0, gr));
-    fixed += 3 + (lowrank ? 2 : 0);
+    fixed += 3 + (lowrank ? (p->r_dense ? 3 : 2) : 0);
     // inner WHILE
     cudaGraphNodeParams ip = {};
     ip.type = cudaGraphNodeTypeConditional;
@@ -1360,6 +1480,8 @@ int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, si
   v.max_inner = prm->max_inner;
   v.halpern = prm->halpern;
   v.quad_kind = p->quad_kind;
+  v.Rd = p->r_dense ? p->R.val : nullptr;
+  v.rk = p->R.rows;
   v.n = p->n;
   v.m = p->m;
   // row shards (aqp_problem_shard): offset every vector to this rank's slice
@@ -1513,6 +1635,7 @@ static int run_eager(aqp_solver *s, int64_t n_iters) {
   const bool diag = p->quad_kind == AQP_QUAD_DIAGONAL;
   const bool lowrank = p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK;
   auto lowrank_pass = [&](int src) -> int {
+    if (p->r_dense) return dense_lowrank(s, src);
     OpRx rx{};
     rx.v = v;
     rx.src = src;
@@ -1603,7 +1726,9 @@ int aqp_solver_check(aqp_solver *s, int with_rays, aqp_check_result *out) {
     AQP_TRY(push_buf(s, PB_DY1));
   }
   if (p->quad_kind != AQP_QUAD_DIAGONAL) {
-    if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
+    if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && p->r_dense) {
+      AQP_TRY(dense_lowrank(s, 2));
+    } else if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
       OpRx rx{}; rx.v = v; rx.src = 2;
       OpRtv rt{}; rt.v = v; rt.src = 2;
       AQP_CUDA(run_spmv(st, p->R, rx, gr));
@@ -1628,7 +1753,9 @@ int aqp_solver_check(aqp_solver *s, int with_rays, aqp_check_result *out) {
         OpChkXRayT<false> q{}; q.v = v; q.j = j; q.which = 1;
         AQP_CUDA(run_elem(st, v.nl, q, gr));
       } else {
-        if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
+        if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && p->r_dense) {
+          AQP_TRY(dense_lowrank(s, 3 + j));
+        } else if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
           OpXRayRx rx{}; rx.v = v; rx.src = 3 + j; rx.j = j;
           OpXRayRtv rt{}; rt.v = v; rt.src = 3 + j; rt.j = j;
           AQP_CUDA(run_spmv(st, p->R, rx, gr));
@@ -1726,7 +1853,8 @@ int aqp_solver_counters(aqp_solver *s, int64_t *out) {
   if (!s || !out) return fail(AQP_EINVAL, "NULL argument");
   out[0] = s->launches_per_iter_fixed;
   out[2] = s->pdl ? 1 : 0;
-  out[1] = s->p->quad_kind == AQP_QUAD_DIAGONAL ? 0 : (s->p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK ? 5 : 3);
+  out[1] = s->p->quad_kind == AQP_QUAD_DIAGONAL ? 0
+           : (s->p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK ? (s->p->r_dense ? 6 : 5) : 3);
   return AQP_OK;
 }
 
@@ -1857,6 +1985,20 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
         OpXPost o{};
         o.v = v;
         AQP_CUDA(run_elem_fin(st, v.nl, o, gr));
+        break;
+      }
+      case 6: {  // dense R x (block partials + fold), source x_t
+        if (!p->r_dense) return fail(AQP_EINVAL, "kernel 6 needs a dense low-rank R");
+        const int nb = (int)dense_rx_blocks(p->n);
+        k_dense_rx<<<nb, kThreads, 0, st>>>(v, 1);
+        k_dense_rx_fold<<<p->R.rows, kThreads, 0, st>>>(v, 1, nb);
+        AQP_CUDA(cudaGetLastError());
+        break;
+      }
+      case 7: {  // dense R'(R x)
+        if (!p->r_dense) return fail(AQP_EINVAL, "kernel 7 needs a dense low-rank R");
+        k_dense_rtv<<<elem_grid(p->n), kThreads, 0, st>>>(v, 1);
+        AQP_CUDA(cudaGetLastError());
         break;
       }
       default: return fail(AQP_EINVAL, "unknown kernel id");

@@ -64,6 +64,18 @@ class DeviceContext:
         return self.torch.from_numpy(np.ascontiguousarray(arr)).to(f"cuda:{self.device}", non_blocking=False)
 
 
+def _full_rows(r) -> bool:
+    """Every row of the CSR holds all columns in order (a dense factor)."""
+    n = r.cols
+    if r.rows == 0 or n == 0 or r.nnz != r.rows * n:
+        return False
+    if not np.array_equal(np.asarray(r.indptr), np.arange(r.rows + 1, dtype=np.int64) * n):
+        return False
+    ar = np.arange(n)
+    idx = np.asarray(r.indices)
+    return all(np.array_equal(idx[i * n:(i + 1) * n], ar) for i in range(r.rows))
+
+
 class DeviceProblem:
     """HBM copy of one QpProblem (reference model.py:124-165)."""
 
@@ -97,7 +109,10 @@ class DeviceProblem:
             if q.kind == "sparse_low_rank":
                 r = q.r
                 d.r_rows = r.rows
-                d.r_indptr, d.r_indices, d.r_data, d.r_nnz = up(r.indptr), up(r.indices), up(r.data), r.nnz
+                d.r_dense = int(_full_rows(r))
+                d.r_indptr = up(r.indptr)
+                d.r_indices = 0 if d.r_dense else up(r.indices)  # dense: the indices are implied
+                d.r_data, d.r_nnz = up(r.data), r.nnz
                 host_r = r.indptr
         d.cost, d.var_lo, d.var_hi = up(p.cost), up(p.var_bounds.lower), up(p.var_bounds.upper)
         d.con_lo, d.con_hi = up(p.con_bounds.lower), up(p.con_bounds.upper)
