@@ -320,7 +320,13 @@ __device__ __forceinline__ void trace_mark(const GridRed &g, unsigned kind) {
 // rows are long enough that a sequential chain would be latency bound).
 // LONG: segment `seg` of `nseg` of one row longer than a tile.  LONGSEQ
 // (strict plans only): a long row summed by one thread in column order.
-enum : int { kItemThread = 0, kItemWarp = 1, kItemLong = 2, kItemLongSeq = 3 };
+// STAGED: a THREAD item whose nonzeros ([k0,k1) <= one tile) are first staged
+// as products in shared memory with coalesced index/value loads and one
+// parallel burst of gathers, then summed one thread per row in column order
+// (bitwise the THREAD order); chosen for matrices whose rows are long enough
+// that the THREAD item's strided per-row loads cost more L1 wavefronts than
+// the staging barrier (mean row length >= AQP_STAGED_MIN, default 8).
+enum : int { kItemThread = 0, kItemWarp = 1, kItemLong = 2, kItemLongSeq = 3, kItemStaged = 4 };
 
 struct __align__(16) PlanItem {
   int row0, row1, k0, k1;

@@ -48,6 +48,10 @@
 
 #include "aqp_common.cuh"
 
+#ifndef AQP_UNIFORM_MIN_BLOCKS
+#define AQP_UNIFORM_MIN_BLOCKS 4
+#endif
+
 namespace aqp {
 
 // Programmatic dependent launch (PDL).  Graph edges between consecutive
@@ -69,6 +73,30 @@ template <class Op>
 struct RowInOf<Op, std::void_t<typename Op::RowIn>> {
   using type = typename Op::RowIn;
   static constexpr bool value = true;
+};
+
+// Per-op tuning of the uniform (THREAD-only) SpMV instantiation:
+//   Op::ROWIN_LATE    load the row's epilogue operands after the gathers
+//                     (frees registers during the gather chain)
+//   Op::UNIFORM_BLOCKS resident 256-thread blocks per SM the register budget
+//                     targets (occupancy vs. per-thread batching)
+// Measured on C2 (scripts/kern_variants.sh): the BB gradient pass is fastest
+// late/6 (50 us vs 56 us early/4), the dual pass P2 early/4.
+template <class Op, class = void>
+struct RowInLateOf {
+  static constexpr bool value = false;
+};
+template <class Op>
+struct RowInLateOf<Op, std::void_t<decltype(Op::ROWIN_LATE)>> {
+  static constexpr bool value = Op::ROWIN_LATE;
+};
+template <class Op, class = void>
+struct UniformBlocksOf {
+  static constexpr int value = AQP_UNIFORM_MIN_BLOCKS;
+};
+template <class Op>
+struct UniformBlocksOf<Op, std::void_t<decltype(Op::UNIFORM_BLOCKS)>> {
+  static constexpr int value = Op::UNIFORM_BLOCKS;
 };
 
 template <class Op, class = void>
@@ -149,14 +177,12 @@ __device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *
 #ifndef AQP_GATHER_BATCH
 #define AQP_GATHER_BATCH 4
 #endif
-#ifndef AQP_UNIFORM_MIN_BLOCKS
-#define AQP_UNIFORM_MIN_BLOCKS 4
-#endif
+
 // UNIFORM: the plan is all THREAD items over [256 b, 256 b + 256) (the common
 // case of short-row matrices, e.g. every C2 pass); the instantiation then
 // carries only the thread-per-row path, which needs far fewer registers
 template <class Op, bool UNIFORM = false>
-__global__ void __launch_bounds__(kThreads, UNIFORM ? AQP_UNIFORM_MIN_BLOCKS : AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
+__global__ void __launch_bounds__(kThreads, UNIFORM ? UniformBlocksOf<Op>::value : AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
   constexpr int NS = Op::NS, NM = Op::NM;
   // static matrix data first: the plan item does not depend on the predecessor
   PlanItem it;
@@ -188,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? AQP_UNIFORM_MIN_BLOCKS : A
     if (r < it.row1) {
       using RowIn = typename RowInOf<Op>::type;
       RowIn rin{};
-      if constexpr (RowInOf<Op>::value) rin = o.load_row(r);
+      if constexpr (RowInOf<Op>::value && !RowInLateOf<Op>::value) rin = o.load_row(r);
       const int b = __ldg(M.ptr + r), e = __ldg(M.ptr + r + 1);
       const int rg = r + M.row_off;  // global row (diagonal position of a symmetric shard)
       double lo = 0.0, up = 0.0;
@@ -224,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? AQP_UNIFORM_MIN_BLOCKS : A
       }
 #endif
       const double val = Op::SYM ? lo + up : up;
+      if constexpr (RowInOf<Op>::value && RowInLateOf<Op>::value) rin = o.load_row(r);
       if constexpr (RowInOf<Op>::value) o.row_in(r, val, rin, acc); else o.row(r, val, acc);
     }
   } else if (UNIFORM) {
@@ -259,6 +286,48 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? AQP_UNIFORM_MIN_BLOCKS : A
         if constexpr (Op::SYM) lo += __shfl_xor_sync(0xffffffffu, lo, off);
       }
       if (lane == 0) o.row(r, Op::SYM ? lo + up : up, acc);
+    }
+  } else if (it.kind == kItemStaged) {
+    // products staged with coalesced loads and one burst of gathers, then
+    // one thread per row sums its slice of the tile in column order
+    const int k0 = it.k0, k1 = it.k1;
+    const int r = it.row0 + threadIdx.x;
+    const bool has = r < it.row1;
+    using RowIn = typename RowInOf<Op>::type;
+    RowIn rin{};
+    int b = 0, e = 0;
+    if (has) {
+      if constexpr (RowInOf<Op>::value) rin = o.load_row(r);
+      b = __ldg(M.ptr + r) - k0;
+      e = __ldg(M.ptr + r + 1) - k0;
+    }
+    constexpr int U = kTileNnz / kThreads;
+    int cs[U];
+    double vs[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + threadIdx.x + u * kThreads;
+      const bool in = k < k1;
+      cs[u] = in ? __ldg(M.idx + k) : 0;
+      vs[u] = in ? __ldg(M.val + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + threadIdx.x + u * kThreads;
+      if (k < k1) {
+        sprod[k - k0] = vs[u] * o.gather(cs[u]);
+        if constexpr (Op::SYM) scol[k - k0] = cs[u];
+      }
+    }
+    __syncthreads();
+    if (has) {
+      const int rg = r + M.row_off;
+      double lo = 0.0, up = 0.0;
+      for (int j = b; j < e; ++j) {
+        if (Op::SYM && scol[j] < rg) lo += sprod[j]; else up += sprod[j];
+      }
+      const double val = Op::SYM ? lo + up : up;
+      if constexpr (RowInOf<Op>::value) o.row_in(r, val, rin, acc); else o.row(r, val, acc);
     }
   } else if (it.kind == kItemLongSeq) {
     if (threadIdx.x == 0) {

@@ -45,7 +45,7 @@ void *Bump::take(size_t bytes) {
 
 // ---------------------------------------------------------------- planner
 template <class P>
-static std::vector<PlanItem> plan_rows(const P *ptr, int64_t rows, bool strict, int *nlongseg) {
+static std::vector<PlanItem> plan_rows(const P *ptr, int64_t rows, bool strict, int *nlongseg, bool staged) {
   std::vector<PlanItem> items;
   int segs = 0;
   int64_t i = 0;
@@ -85,14 +85,20 @@ static std::vector<PlanItem> plan_rows(const P *ptr, int64_t rows, bool strict, 
     // one thread per row, sequential in column order (no shared memory)
     const int64_t row_max = strict ? (int64_t)kTileNnz : (int64_t)kThreadRowMax;
     const int64_t start = i;
-    while (i < rows && i - start < kThreads && (int64_t)(ptr[i + 1] - ptr[i]) <= row_max) ++i;
+    if (staged) {  // STAGED item: <= 256 short rows whose nonzeros fit one tile
+      while (i < rows && i - start < kThreads && (int64_t)(ptr[i + 1] - ptr[i]) <= row_max &&
+             (int64_t)(ptr[i + 1] - ptr[start]) <= (int64_t)kTileNnz)
+        ++i;
+    } else {
+      while (i < rows && i - start < kThreads && (int64_t)(ptr[i + 1] - ptr[i]) <= row_max) ++i;
+    }
     if (i > start) {
       PlanItem it{};
       it.row0 = (int)start;
       it.row1 = (int)i;
       it.k0 = (int)ptr[start];
       it.k1 = (int)ptr[i];
-      it.kind = kItemThread;
+      it.kind = staged ? kItemStaged : kItemThread;
       items.push_back(it);
       continue;
     }
@@ -239,10 +245,19 @@ static int counts_to_ptr(int *counts, int rows, int *ptr_out, void *tmp, size_t 
 
 int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *host_ptr64, bool strict,
                 PlanItem *plan_dev, int64_t plan_cap, double *seg_part, unsigned *seg_ticket,
-                int64_t seg_cap) {
+                int64_t seg_cap, bool may_stage) {
   int nlong = 0;
-  std::vector<PlanItem> items = host_ptr64 ? plan_rows(host_ptr64, M.rows, strict, &nlong)
-                                           : plan_rows(host_ptr32, M.rows, strict, &nlong);
+  // STAGED items for matrices with long-enough rows (see kItemStaged)
+  // measured on C5 (n = m = 5e7, 10 nnz / row): STAGED speeds the A' pass
+  // (P1, 2.80 -> 2.55 ms) but slows the A pass (P2, whose epilogue operands
+  // are held across the staging barrier: 2.51 -> 2.86 ms), so only A' stages
+  double staged_min = may_stage ? 8.0 : 1e300;
+  if (const char *e = getenv("AQP_STAGED_MIN")) staged_min = atof(e);
+  const int64_t nnz_rows = M.rows > 0 ? (host_ptr64 ? host_ptr64[M.rows] - host_ptr64[0]
+                                                    : (int64_t)host_ptr32[M.rows] - host_ptr32[0]) : 0;
+  const bool staged = !strict && M.rows > 0 && (double)nnz_rows >= staged_min * (double)M.rows;
+  std::vector<PlanItem> items = host_ptr64 ? plan_rows(host_ptr64, M.rows, strict, &nlong, staged)
+                                           : plan_rows(host_ptr32, M.rows, strict, &nlong, staged);
   if ((int64_t)items.size() > plan_cap) return fail(AQP_ENOMEM, "plan capacity exceeded");
   if (nlong > seg_cap) return fail(AQP_ENOMEM, "segment capacity exceeded");
   AQP_CUDA(cudaMemcpyAsync(plan_dev, items.data(), items.size() * sizeof(PlanItem), cudaMemcpyHostToDevice,
@@ -251,7 +266,7 @@ int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *h
   M.plan = plan_dev;
   M.nitems = (int)items.size();
   bool warp_items = false;
-  for (const PlanItem &it : items) warp_items |= it.kind == kItemWarp;
+  for (const PlanItem &it : items) warp_items |= it.kind == kItemWarp || it.kind == kItemStaged;
   M.smem_bytes = warp_items ? kTileNnz * (int)(sizeof(double) + sizeof(int)) : 0;
   // uniform plans let the kernel derive its rows from blockIdx (no plan load)
   bool uniform = M.rows > 0;
@@ -292,7 +307,8 @@ int upload_csr(aqp_ctx *ctx, CsrStore &s, DevCsr &M, int64_t rows, int64_t cols,
   M.ptr = s.ptr;
   M.idx = s.idx;
   M.val = s.val;
-  return finish_plan(ctx, M, nullptr, host_ptr, strict, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap);
+  return finish_plan(ctx, M, nullptr, host_ptr, strict, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap,
+                     false);
 }
 
 // Transpose of an uploaded CSR (src) into storage t (rows = src.cols).
@@ -334,7 +350,8 @@ int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool 
   std::vector<int> hptr(rows_t + 1);
   AQP_CUDA(cudaMemcpyAsync(hptr.data(), t.ptr, (rows_t + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
   AQP_CUDA(cudaStreamSynchronize(st));
-  return finish_plan(ctx, T, hptr.data(), nullptr, strict, t.plan, t.plan_cap, t.seg_part, t.seg_ticket, t.seg_cap);
+  return finish_plan(ctx, T, hptr.data(), nullptr, strict, t.plan, t.plan_cap, t.seg_part, t.seg_ticket, t.seg_cap,
+                     true);
 }
 
 // Full symmetric expansion of an uploaded upper-triangle CSR U (n x n).
@@ -386,7 +403,8 @@ int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool s
   std::vector<int> hptr(n + 1);
   AQP_CUDA(cudaMemcpyAsync(hptr.data(), f.ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
   AQP_CUDA(cudaStreamSynchronize(st));
-  return finish_plan(ctx, F, hptr.data(), nullptr, strict, f.plan, f.plan_cap, f.seg_part, f.seg_ticket, f.seg_cap);
+  return finish_plan(ctx, F, hptr.data(), nullptr, strict, f.plan, f.plan_cap, f.seg_part, f.seg_ticket, f.seg_cap,
+                     false);
 }
 
 size_t transpose_scratch_bytes(int64_t nnz, int64_t cols) {
@@ -621,7 +639,7 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
 // Restrict the SpMV passes to rows [r0, r1) of M: the row pointers are a
 // window of the full array (absolute nonzero offsets, so idx/val stay put)
 // and the work plan is rebuilt for the local rows.
-static int slice_rows(aqp_ctx *ctx, DevCsr &M, CsrStore &s, int64_t r0, int64_t r1, int row_off) {
+static int slice_rows(aqp_ctx *ctx, DevCsr &M, CsrStore &s, int64_t r0, int64_t r1, int row_off, bool may_stage) {
   std::vector<int> hptr((size_t)(r1 - r0 + 1));
   AQP_CUDA(cudaMemcpyAsync(hptr.data(), M.ptr + r0, hptr.size() * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   AQP_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -630,7 +648,8 @@ static int slice_rows(aqp_ctx *ctx, DevCsr &M, CsrStore &s, int64_t r0, int64_t 
   M.nnz = (int64_t)hptr.back() - hptr.front();
   M.row_off = row_off;
   AQP_CUDA(cudaMemsetAsync(s.seg_ticket, 0, s.seg_cap * sizeof(unsigned), ctx->stream));
-  return finish_plan(ctx, M, hptr.data(), nullptr, false, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap);
+  return finish_plan(ctx, M, hptr.data(), nullptr, false, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap,
+                     may_stage);
 }
 
 int aqp_problem_shard(aqp_problem *p, const aqp_shard *sh) {
@@ -644,9 +663,10 @@ int aqp_problem_shard(aqp_problem *p, const aqp_shard *sh) {
   if (sh->nranks > 1 && p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK)
     return fail(AQP_EINVAL, "low-rank Q is not row-sharded (R x needs every column)");
   AQP_CUDA(cudaSetDevice(p->ctx->device));
-  AQP_TRY(slice_rows(p->ctx, p->A, p->sA, sh->m0, sh->m1, 0));
-  AQP_TRY(slice_rows(p->ctx, p->At, p->sAt, sh->n0, sh->n1, 0));
-  if (p->quad_kind == AQP_QUAD_SPARSE) AQP_TRY(slice_rows(p->ctx, p->Q, p->sQ, sh->n0, sh->n1, (int)sh->n0));
+  AQP_TRY(slice_rows(p->ctx, p->A, p->sA, sh->m0, sh->m1, 0, false));
+  AQP_TRY(slice_rows(p->ctx, p->At, p->sAt, sh->n0, sh->n1, 0, true));
+  if (p->quad_kind == AQP_QUAD_SPARSE)
+    AQP_TRY(slice_rows(p->ctx, p->Q, p->sQ, sh->n0, sh->n1, (int)sh->n0, false));
   p->rank = sh->rank;
   p->nranks = sh->nranks;
   p->n0 = sh->n0;

@@ -145,6 +145,8 @@ struct Combine {
 struct OpP1Bb {
   static constexpr int NS = 0, NM = 0;
   static constexpr bool SYM = false, FINAL = false;
+  static constexpr bool ROWIN_LATE = true;
+  static constexpr int UNIFORM_BLOCKS = 6;
   SV v;
   const double *y;
   const double *x;
@@ -221,6 +223,8 @@ template <bool INIT>
 struct OpGrad {
   static constexpr int NS = INIT ? 4 : 7, NM = 0;
   static constexpr bool SYM = true, FINAL = true, SPLIT = true;
+  static constexpr bool ROWIN_LATE = true;   // see aqp_kernels.cuh RowInLateOf
+  static constexpr int UNIFORM_BLOCKS = 6;
   SV v;
   const double *xt, *cen, *xo, *go;
   double *gt;
