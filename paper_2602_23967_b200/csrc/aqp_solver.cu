@@ -509,6 +509,83 @@ struct OpRtv {
 // order), R'(Rx) is a streaming pass whose entry i sums k products in row
 // order -- bitwise the order of the reference's csr_matvec_t over R
 // (_core.pyx:45-59).  Both read R once: 8 k n bytes per pass.
+#ifndef AQP_DENSE_RX_V1
+// R x, every warp on every row: a block owns kRxCols columns; warp w owns the
+// column slice [w*S, (w+1)*S) (S = kRxCols / kWarps) of the chunk and walks
+// all k rows over it (coalesced 128-bit loads of R, x from shared memory),
+// folds each row with a fixed xor tree into smem[row][warp], and the block
+// sums the kWarps slice values of a row in warp order.  Every warp does the
+// same work for any k (no row imbalance), and 2048-column chunks keep 8
+// blocks resident per SM (2.06 waves at C3 instead of 1.18).
+constexpr int kRxCols = 2048;
+constexpr int kRxMaxRows = 128;  // rows handled per pass over the chunk (smem [kRxMaxRows][kWarps])
+inline int64_t dense_rx_blocks(int64_t n) { return std::max<int64_t>((n + kRxCols - 1) / kRxCols, 1); }
+__device__ __forceinline__ bool cand_valid(const Ctrl *ct, int j, double norm);
+__device__ __forceinline__ const double *lowrank_src(const SV &v, int src) {
+  const Ctrl *ct = v.ctrl;
+  return src == 0 ? pick3(v.xbb, 0) : src == 1 ? pick3(v.xbb, ct->bb_new) : src == 2 ? v.xeval : pick2(v.dx, src - 3);
+}
+// x-ray candidates only when the cheap test passed (certify.py:148-157)
+__device__ __forceinline__ bool lowrank_skip(const SV &v, int src) {
+  if (src < 3) return false;
+  const Ctrl *ct = v.ctrl;
+  const int j = src - 3;
+  const double *xr = ct->red + R_XR + 5 * j;
+  return !(cand_valid(ct, j, xr[0]) && xr[1] < -v.eps_tol);
+}
+
+__global__ void __launch_bounds__(kThreads) k_dense_rx(SV v, int src) {
+  constexpr int S = kRxCols / kWarps;  // columns per warp slice (256)
+  __shared__ __align__(16) double xs[kRxCols];
+  __shared__ double red[kRxMaxRows][kWarps + 1];
+  pdl_wait();
+  if (lowrank_skip(v, src)) return;
+  const double *x = lowrank_src(v, src);
+  const int64_t n = v.n;
+  const int64_t j0 = (int64_t)blockIdx.x * kRxCols;
+  const int len = (int)min((int64_t)kRxCols, n - j0);
+  for (int t = threadIdx.x; t < kRxCols; t += kThreads) xs[t] = t < len ? x[j0 + t] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c0 = warp * S;                        // this warp's slice of the chunk
+  const int clen = max(0, min(S, len - c0));
+  const bool vec = (n & 1) == 0 && clen == S;     // full slice, 16-byte aligned rows
+  for (int kb = 0; kb < v.rk; kb += kRxMaxRows) {
+    const int kend = min(v.rk, kb + kRxMaxRows);
+    for (int kk = kb; kk < kend; ++kk) {
+      const double *row = v.Rd + (int64_t)kk * n + j0 + c0;
+      double a0 = 0.0, a1 = 0.0;
+      if (vec) {
+        const double2 *r2 = reinterpret_cast<const double2 *>(row);
+        const double2 *x2 = reinterpret_cast<const double2 *>(xs + c0);
+#pragma unroll
+        for (int u = 0; u < S / 64; ++u) {
+          const double2 r = __ldcs(r2 + lane + 32 * u);  // streamed once per pass
+          const double2 q = x2[lane + 32 * u];
+          a0 += r.x * q.x;
+          a1 += r.y * q.y;
+        }
+      } else {
+        for (int u = lane; u < clen; u += 32) a0 += __ldcs(row + u) * xs[c0 + u];
+      }
+      double a = a0 + a1;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      if (lane == 0) red[kk - kb][warp] = a;
+    }
+    __syncthreads();
+    for (int kk = kb + threadIdx.x; kk < kend; kk += kThreads) {
+      double a = red[kk - kb][0];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) a += red[kk - kb][w];
+      v.rxpart[(size_t)kk * gridDim.x + blockIdx.x] = a;
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+
+#else
 constexpr int kRxCols = 4096;  // columns per block of the R x pass (32 KB of x in smem)
 inline int64_t dense_rx_blocks(int64_t n) { return std::max<int64_t>((n + kRxCols - 1) / kRxCols, 1); }
 __device__ __forceinline__ bool cand_valid(const Ctrl *ct, int j, double norm);
@@ -564,6 +641,8 @@ __global__ void __launch_bounds__(kThreads) k_dense_rx(SV v, int src) {
   }
   pdl_trigger();
 }
+
+#endif
 
 // rx[k] = fold of the k-th row's block partials (block order, fixed tree)
 __global__ void __launch_bounds__(kThreads) k_dense_rx_fold(SV v, int src, int nb) {
