@@ -44,6 +44,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -121,6 +123,13 @@ def dist_init():
     return world, rank, local
 
 
+def workload_name(p) -> str:
+    nnz_q = 2 * p.quad.upper.nnz - int(np.count_nonzero(p.quad.upper.indices == np.repeat(
+        np.arange(p.n), np.diff(p.quad.upper.indptr))))
+    return (f"C2 lasso-style QP n={p.n} m={p.m} nnz(A)={p.constraint_matrix.nnz} nnz(Q_full)={nnz_q} "
+            f"(BASELINE configs[1])")
+
+
 def problem_bytes(p) -> int:
     a, q = p.constraint_matrix, p.quad
     arrs = [a.indptr, a.indices, a.data, p.cost, p.var_bounds.lower, p.var_bounds.upper, p.con_bounds.lower,
@@ -151,12 +160,18 @@ def run_reference(args, world, rank):
     threads = os.cpu_count() or 1
     r = cpu_baseline(spec, max(args.warmup, 1), args.steps, threads)
     value = r["inner"] / r["seconds"]
+    from paper_2602_23967_b200 import generators
+
+    prob = generators.lasso_style_qp(SPEC_N, SPEC_M, seed=0)
+    workload = workload_name(prob)
     line = {
         "metric": METRIC, "value": value, "unit": "inner_iters/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C2 lasso-style QP n={SPEC_N} m={SPEC_M} (BASELINE configs[1])",
-                   "step": "one outer PDHG iteration (BB inner solve included)", "eps_tol": EPS},
+        "scaling": "strong" if args.gpus > 1 and not args.replicas else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload,
+                   "step": "one outer PDHG iteration (BB inner solve included) of the reference CPU solver",
+                   "eps_tol": EPS},
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "inner_iters/s", "cores": threads, "kind": r["kind"],
                          "sample": f"outer iterations {max(args.warmup,1)}..{max(args.warmup,1)+args.steps} of the C2 solve "
@@ -269,8 +284,7 @@ def run_ours(args, world, rank, local):
         "ms_per_step": ms_max / K if K else None, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C2 lasso-style QP n={n} m={m} nnz(A)={problem.constraint_matrix.nnz} "
-                               f"nnz(Q_full)={nnz_q} (BASELINE configs[1])",
+        "config": {"workload": workload_name(problem),
                    "step": f"one certification window = {CHECK_EVERY} outer iterations + device check",
                    "eps_tol": EPS,
                    "parallelism": f"rowshard{world}" if sharded else ("replicas" if world > 1 else "single"),

@@ -134,18 +134,21 @@ __device__ __forceinline__ void block_reduce(RedVals<NS, NM> &v, double *smem /*
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    // warps outer, slots inner: every slot still adds its warp values in
+    // warp order (bitwise the slot-by-slot loop), but the NS + NM dependent
+    // chains interleave instead of running back to back -- with 32 warps and
+    // 7 slots that is 32 instead of 224 dependent shared-load + add steps
+    // (the BB fold kernel's critical path, ~3.5 us, device trace)
     const int nw = (int)(blockDim.x >> 5);
 #pragma unroll
-    for (int i = 0; i < NS; ++i) {
-      double a = smem[i];
-      for (int w = 1; w < nw; ++w) a += smem[w * NT + i];
-      v.s[i] = a;
-    }
+    for (int i = 0; i < NS; ++i) v.s[i] = smem[i];
 #pragma unroll
-    for (int i = 0; i < NM; ++i) {
-      double a = smem[NS + i];
-      for (int w = 1; w < nw; ++w) a = nanmax(a, smem[w * NT + NS + i]);
-      v.m[i] = a;
+    for (int i = 0; i < NM; ++i) v.m[i] = smem[NS + i];
+    for (int w = 1; w < nw; ++w) {
+#pragma unroll
+      for (int i = 0; i < NS; ++i) v.s[i] += smem[w * NT + i];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) v.m[i] = nanmax(v.m[i], smem[w * NT + NS + i]);
     }
   }
   __syncthreads();
