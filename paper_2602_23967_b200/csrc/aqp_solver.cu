@@ -229,10 +229,11 @@ struct OpGrad {
   const double *xt, *cen, *xo, *go;
   double *gt;
   double tau;
+  int cond;  // second half of an unrolled BB body: run only while the loop continues
   // no halted test: a halted iteration closes the outer WHILE (OpP2), so no
   // later launch of the window runs; a load + branch here would serialise
   // every block's first memory access behind a round trip
-  __device__ bool skip() const { return false; }
+  __device__ bool skip() const { return cond && !v.ctrl->bb_cont; }
   __device__ void prepare() {
     const Ctrl *ct = v.ctrl;
     xt = INIT ? pick3(v.xbb, 0) : pick3(v.xbb, ct->bb_new);
@@ -353,10 +354,11 @@ struct OpStep {
   const double *xo, *go;
   double *xn;
   double alpha;
+  int cond;  // as OpGrad::cond
   // no halted test: a halted iteration closes the outer WHILE (OpP2), so no
   // later launch of the window runs; a load + branch here would serialise
   // every block's first memory access behind a round trip
-  __device__ bool skip() const { return false; }
+  __device__ bool skip() const { return cond && !v.ctrl->bb_cont; }
   __device__ void prepare() {
     const Ctrl *ct = v.ctrl;
     xo = pick3(v.xbb, ct->bb_cur);
@@ -1403,14 +1405,25 @@ int build_graph(aqp_solver *s) {
     last.kernel = false;
     cudaGraph_t ib = ip.conditional.phGraph_out[0];
     GNode il;
-    OpStep st{};
-    st.v = v;
-    AQP_CUDA(node_elem(ib, il, v.nl, st, gr));
-    if (s->shard) AQP_CUDA(node_barrier(ib, il, gr));
-    if (lowrank) AQP_TRY(add_lowrank(s, ib, il, 1));
-    OpGrad<false> gg{};
-    gg.v = v;
-    AQP_CUDA(node_spmv_fin(ib, il, p->Q, gg, gr));
+    // The body holds `unroll` BB iterations; copies after the first run only
+    // while the loop continues (their kernels exit at once otherwise).  A
+    // WHILE-node iteration boundary costs ~6.5 us (device trace: fold end ->
+    // next step start) against ~1 us for a programmatic edge inside the body.
+    int unroll = 2;
+    if (const char *e = getenv("AQP_BB_UNROLL")) unroll = std::max(1, atoi(e));
+    if (lowrank) unroll = 1;  // the low-rank passes have no conditional exit
+    for (int u = 0; u < unroll; ++u) {
+      OpStep st{};
+      st.v = v;
+      st.cond = u > 0;
+      AQP_CUDA(node_elem(ib, il, v.nl, st, gr));
+      if (s->shard) AQP_CUDA(node_barrier(ib, il, gr));
+      if (lowrank) AQP_TRY(add_lowrank(s, ib, il, 1));
+      OpGrad<false> gg{};
+      gg.v = v;
+      gg.cond = u > 0;
+      AQP_CUDA(node_spmv_fin(ib, il, p->Q, gg, gr));
+    }
     OpXPost xp{};
     xp.v = v;
     AQP_CUDA(node_elem_fin(body, last, v.nl, xp, gr));
