@@ -435,16 +435,6 @@ static __global__ void k_comm_barrier(GridRed g) {
   pdl_trigger();
 }
 
-// replicate this rank's slice [0, len) of a gathered vector (pointer already
-// offset to the slice) into every peer's copy
-static __global__ void __launch_bounds__(kThreads) k_comm_push(const double *p, int64_t len, GridRed g) {
-  pdl_wait();
-  const Comm &c = g.comm;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
-    peer_put(c, const_cast<double *>(p), i, p[i]);
-  pdl_trigger();
-}
-
 // grid of an elementwise pass: a pure function of n (so reductions are
 // reproducible), at most 8 resident 256-thread blocks on each of 148 SMs
 inline int elem_grid(int64_t n) {
