@@ -87,6 +87,21 @@ struct SV {
 };
 
 
+// Gather of a vector the solve itself writes.  AQP_GATHER_NC=1 uses the
+// non-coherent read-only path (ld.global.nc); the default plain ld.global is
+// coherent, so the same ops can run inside a persistent kernel whose phases
+// are separated by grid barriers instead of kernel boundaries.
+#ifndef AQP_GATHER_NC
+#define AQP_GATHER_NC 0
+#endif
+__device__ __forceinline__ double gld(const double *p) {
+#if AQP_GATHER_NC
+  return __ldg(p);
+#else
+  return *p;
+#endif
+}
+
 // slot selection without dynamic indexing (keeps the op out of local memory)
 template <class T>
 __host__ __device__ __forceinline__ T pick3(T const (&a)[3], int i) { return i == 0 ? a[0] : (i == 1 ? a[1] : a[2]); }
@@ -158,7 +173,7 @@ struct OpP1Bb {
     y = pick3(v.ys, v.ctrl->ycur) - v.yoff;
     x = pick3(v.xs, v.ctrl->xcur);
   }
-  __device__ double gather(int c) const { return __ldg(y + c); }
+  __device__ double gather(int c) const { return gld(y + c); }
   struct RowIn {
     double c, x, lo, hi;
   };
@@ -196,7 +211,7 @@ struct OpP1Diag {
     tau = ct->tau;
     cb.init(v);
   }
-  __device__ double gather(int c) const { return __ldg(y + c); }
+  __device__ double gather(int c) const { return gld(y + c); }
   __device__ void row(int r, double s, RedVals<1, 0> &acc) const {
     const double lin = v.c[r] + s;
     const double xk = x[r];
@@ -243,7 +258,7 @@ struct OpGrad {
     cen = pick3(v.xs, ct->xcur);
     tau = ct->tau;
   }
-  __device__ double gather(int c) const { return __ldg(xt - v.xoff + c); }
+  __device__ double gather(int c) const { return gld(xt - v.xoff + c); }
   // epilogue operands of row r, loaded ahead of the SpMV tile (THREAD tiles)
   struct RowIn {
     double x, c, l, lo, hi, xo, go, rt;
@@ -429,7 +444,7 @@ struct OpP2 {
     sigma = ct->sigma;
     cb.init(v);
   }
-  __device__ double gather(int c) const { return halted ? 0.0 : __ldg(v.xbar - v.xoff + c); }
+  __device__ double gather(int c) const { return halted ? 0.0 : gld(v.xbar - v.xoff + c); }
   struct RowIn {
     double y, lo, hi, anc, blk, prev;
   };
@@ -487,7 +502,7 @@ struct OpRx {
     x = src == 0 ? pick3(v.xbb, 0) : src == 1 ? pick3(v.xbb, ct->bb_new) : src == 2 ? v.xeval : pick2(v.dx, src - 3);
     x -= v.xoff;
   }
-  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ double gather(int c) const { return gld(x + c); }
   __device__ void row(int r, double s, RedVals<0, 0> &) const { v.rx[r] = s; }
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
@@ -499,7 +514,7 @@ struct OpRtv {
   int src;
   __device__ bool skip() const { return false; }
   __device__ void prepare() {}
-  __device__ double gather(int c) const { return __ldg(v.rx + c); }
+  __device__ double gather(int c) const { return gld(v.rx + c); }
   __device__ void row(int r, double s, RedVals<0, 0> &) const { v.rtv[r] = s; }
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
@@ -793,7 +808,7 @@ struct OpChkA {
       ok[j] = rays && cand_valid(ct, j, nrm[j]);
     }
   }
-  __device__ double gather(int c) const { return __ldg(v.xeval - v.xoff + c); }
+  __device__ double gather(int c) const { return gld(v.xeval - v.xoff + c); }
   __device__ void row(int r, double s, RedVals<6, 1> &acc) const {
     acc.m[0] = nanmax(acc.m[0], absd(s - clip(s, v.clo[r], v.chi[r])));
 #pragma unroll
@@ -835,7 +850,7 @@ struct OpStore {
         : src == 2 ? pick3(v.xbb, 1) - v.xoff : v.tm - v.yoff;
     out = dst == 0 ? v.qx : dst == 1 ? v.aty : dst == 2 ? v.tm : pick3(v.xbb, 2);
   }
-  __device__ double gather(int c) const { return __ldg(x + c); }
+  __device__ double gather(int c) const { return gld(x + c); }
   __device__ void row(int r, double s, RedVals<1, 0> &acc) const {
     const double o = dst == 0 ? quad_row(v, r, s) : s;
     out[r] = o;
@@ -925,7 +940,7 @@ struct OpChkYRay {
     return !cand_valid(ct, j, ct->red[R_YR + 9 * j]);
   }
   __device__ void prepare() { ray = pick2(v.dy, j) - v.yoff; }
-  __device__ double gather(int c) const { return __ldg(ray + c); }
+  __device__ double gather(int c) const { return gld(ray + c); }
   __device__ void row(int r, double s, RedVals<3, 2> &acc) const {
     const double p = cone_proj(s, v.cone_r[r]);
     acc.m[0] = nanmax(acc.m[0], absd(s - p));
@@ -958,7 +973,7 @@ struct OpChkXRay {
     return !(cand_valid(ct, j, xr[0]) && xr[1] < -v.eps_tol);
   }
   __device__ void prepare() { d = pick2(v.dx, j); }
-  __device__ double gather(int c) const { return __ldg(d - v.xoff + c); }
+  __device__ double gather(int c) const { return gld(d - v.xoff + c); }
   __device__ void row(int r, double s, RedVals<0, 1> &acc) const {
     if (which == 0) {
       acc.m[0] = nanmax(acc.m[0], absd(s - cone_proj(s, v.recc_s[r])));
