@@ -181,31 +181,13 @@ __device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *
 // UNIFORM: the plan is all THREAD items over [256 b, 256 b + 256) (the common
 // case of short-row matrices, e.g. every C2 pass); the instantiation then
 // carries only the thread-per-row path, which needs far fewer registers
-template <class Op, bool UNIFORM = false>
-__global__ void __launch_bounds__(kThreads, UNIFORM ? UniformBlocksOf<Op>::value : AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
-  constexpr int NS = Op::NS, NM = Op::NM;
-  // static matrix data first: the plan item does not depend on the predecessor
-  PlanItem it;
-  if (UNIFORM || M.uniform) {
-    it.kind = kItemThread;
-    it.row0 = blockIdx.x * kThreads;
-    it.row1 = min(it.row0 + kThreads, M.rows);
-  } else {
-    it = M.plan[blockIdx.x];
-  }
-  pdl_wait();
-  trace_mark(g, 0);
-  if (op.skip()) return;
-  Op o = op;
-  o.prepare();
-  // WARP-item staging buffer: dynamic, launched with M.smem_bytes (0 when the
-  // matrix has no WARP items, so THREAD-only passes keep full occupancy)
-  extern __shared__ double dyn_smem[];
-  double *sprod = dyn_smem;
-  int *scol = reinterpret_cast<int *>(dyn_smem + kTileNnz);
-  __shared__ double sred[kWarps * kMaxRed];
-  RedVals<NS, NM> acc;
-  acc.zero();
+// One plan item of an SpMV pass with op `o`: the block's rows are summed
+// (THREAD / STAGED / WARP / LONGSEQ / LONG, see the file header) and their
+// epilogue accumulates into `acc`.  Shared by spmv_op (one item per block) and
+// the persistent small-problem window kernel (items looped over a resident grid).
+template <class Op, bool UNIFORM>
+__device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, const Op &o,
+                                          RedVals<Op::NS, Op::NM> &acc, double *sprod, int *scol, double *sred) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   if (it.kind == kItemThread) {
@@ -375,6 +357,34 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? UniformBlocksOf<Op>::value
       }
     }
   }
+}
+
+template <class Op, bool UNIFORM = false>
+__global__ void __launch_bounds__(kThreads, UNIFORM ? UniformBlocksOf<Op>::value : AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
+  constexpr int NS = Op::NS, NM = Op::NM;
+  // static matrix data first: the plan item does not depend on the predecessor
+  PlanItem it;
+  if (UNIFORM || M.uniform) {
+    it.kind = kItemThread;
+    it.row0 = blockIdx.x * kThreads;
+    it.row1 = min(it.row0 + kThreads, M.rows);
+  } else {
+    it = M.plan[blockIdx.x];
+  }
+  pdl_wait();
+  trace_mark(g, 0);
+  if (op.skip()) return;
+  Op o = op;
+  o.prepare();
+  // WARP-item staging buffer: dynamic, launched with M.smem_bytes (0 when the
+  // matrix has no WARP items, so THREAD-only passes keep full occupancy)
+  extern __shared__ double dyn_smem[];
+  double *sprod = dyn_smem;
+  int *scol = reinterpret_cast<int *>(dyn_smem + kTileNnz);
+  __shared__ double sred[kWarps * kMaxRed];
+  RedVals<NS, NM> acc;
+  acc.zero();
+  spmv_item<Op, UNIFORM>(M, it, o, acc, sprod, scol, sred);
   pdl_trigger();
   if constexpr (Op::FINAL) {
     if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred)) o.finalize(acc);
@@ -437,7 +447,7 @@ static __global__ void k_comm_barrier(GridRed g) {
 
 // grid of an elementwise pass: a pure function of n (so reductions are
 // reproducible), at most 8 resident 256-thread blocks on each of 148 SMs
-inline int elem_grid(int64_t n) {
+__host__ __device__ inline int elem_grid(int64_t n) {
   int64_t b = (n + kThreads - 1) / kThreads;
   if (b < 1) b = 1;
   if (b > 148 * 8) b = 148 * 8;
