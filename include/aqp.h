@@ -239,6 +239,12 @@ int aqp_solver_destroy(aqp_solver *s);
  * same calls in the same order. */
 int aqp_solver_exchange_region(aqp_solver *s, void **base, size_t *bytes);
 int aqp_solver_connect(aqp_solver *s, void *const *peer_bases, int nranks);
+/* Optional, before aqp_solver_connect: the gather halos of every rank.  Rank
+ * k gathers x only in [x_lohi[2k], x_lohi[2k+1]) (columns of its rows of A
+ * and Q) and y only in [y_lohi[2k], y_lohi[2k+1]) (columns of its rows of
+ * A'); producers then store to peer k only entries inside k's range.
+ * Default: the whole vector (every peer gets everything). */
+int aqp_solver_set_halos(aqp_solver *s, const int64_t *x_lohi, const int64_t *y_lohi, int nranks);
 /* x0 = clamp(0), y0 = 0, all round/anchor buffers <- (x0, y0) (engine.py:174-204) */
 int aqp_solver_init(aqp_solver *s, const aqp_scalars *sc);
 int aqp_solver_set_scalars(aqp_solver *s, const aqp_scalars *sc);

@@ -130,6 +130,7 @@ SIGNATURES = {
     "aqp_problem_shard": (C.c_int, [_P, C.POINTER(Shard)]),
     "aqp_solver_exchange_region": (C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_size_t)]),
     "aqp_solver_connect": (C.c_int, [_P, C.POINTER(_P), C.c_int]),
+    "aqp_solver_set_halos": (C.c_int, [_P, c_int64_p, c_int64_p, C.c_int]),
     "aqp_ipc_get_handle": (C.c_int, [_P, _P, C.POINTER(C.c_size_t)]),
     "aqp_ipc_open": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
     "aqp_ipc_close": (C.c_int, [_P, C.c_size_t]),

@@ -182,6 +182,12 @@ struct Comm {
   CommBlock *cb = nullptr;
   unsigned long long timeout_ns = 30000000000ull;  // a peer that never arrives: give up, flag, carry on
   long long delta[kMaxRanks] = {};  // byte offset local -> rank k's mapping of the same buffer
+  // Halo ranges: rank k only ever gathers x entries in [xlo[k], xhi[k]) (the
+  // columns of its rows of A and Q) and y entries in [ylo[k], yhi[k]) (the
+  // columns of its rows of A'), so a producer stores to peer k only what
+  // falls in k's range -- for a banded C5 that is a boundary strip instead of
+  // the whole slice.  Defaults: everything.
+  long long xlo[kMaxRanks] = {}, xhi[kMaxRanks] = {}, ylo[kMaxRanks] = {}, yhi[kMaxRanks] = {};
 };
 
 // c.delta[k] for a run-time k without indexing the kernel-parameter array
@@ -205,6 +211,16 @@ __device__ __forceinline__ void peer_put(const Comm &c, double *p, int64_t i, do
   for (int k = 0; k < kMaxRanks; ++k)
     if (k < c.nranks && k != c.rank)
       *reinterpret_cast<double *>(reinterpret_cast<char *>(p + i) + c.delta[k]) = val;
+}
+// ... only to the peers that gather global entry g (x side: side = 0, y side: 1)
+__device__ __forceinline__ void peer_put_halo(const Comm &c, int side, double *p, int64_t i, int64_t g, double val) {
+  if (c.nranks <= 1) return;
+#pragma unroll
+  for (int k = 0; k < kMaxRanks; ++k) {
+    const long long lo = side ? c.ylo[k] : c.xlo[k], hi = side ? c.yhi[k] : c.xhi[k];
+    if (k < c.nranks && k != c.rank && g >= lo && g < hi)
+      *reinterpret_cast<double *>(reinterpret_cast<char *>(p + i) + c.delta[k]) = val;
+  }
 }
 
 __device__ __forceinline__ unsigned long long global_ns_() {

@@ -184,7 +184,7 @@ struct OpP1Bb {
     v.lin[r] = in.c + s;                            // engine.py:214 cost + A'y
     const double x0 = clip(in.x, in.lo, in.hi);       // inner.py:94
     v.xbb[0][r] = x0;
-    peer_put(v.cm, v.xbb[0], r, x0);                  // G0 gathers x0 on every rank
+    peer_put_halo(v.cm, 0, v.xbb[0], r, r + v.xoff, x0);                  // G0 gathers x0 on every rank
   }
   __device__ void row(int r, double s, RedVals<0, 0> &acc) const { row_in(r, s, load_row(r), acc); }
   __device__ void finalize(const RedVals<0, 0> &) const {}
@@ -220,7 +220,7 @@ struct OpP1Diag {
     const double xp = clip((xk - tau * lin) / (1.0 + tau * v.qd[r]), v.vlo[r], v.vhi[r]);  // _core.pyx:127
     const double xb = 2.0 * xp + (-1.0) * xk;                                               // axpby
     v.xbar[r] = xb;
-    peer_put(v.cm, v.xbar, r, xb);
+    peer_put_halo(v.cm, 0, v.xbar, r, r + v.xoff, xb);
     const double z = cb(xp, v.anc_x, xprev, r);
     const double d = z - xk;
     acc.s[0] += d * d;
@@ -386,7 +386,7 @@ struct OpStep {
   __device__ void elem(int64_t i, RedVals<0, 0> &) const {
     const double x = clip(xo[i] - alpha * go[i], v.vlo[i], v.vhi[i]);
     xn[i] = x;
-    peer_put(v.cm, xn, i, x);  // the next G pass gathers x_t on every rank
+    peer_put_halo(v.cm, 0, xn, i, i + v.xoff, x);  // the next G pass gathers x_t on every rank
   }
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
@@ -415,7 +415,7 @@ struct OpXPost {
     const double p = xp[i], xk = x[i];
     const double xb = 2.0 * p + (-1.0) * xk;
     v.xbar[i] = xb;
-    peer_put(v.cm, v.xbar, i, xb);
+    peer_put_halo(v.cm, 0, v.xbar, i, i + v.xoff, xb);
     const double z = cb(p, v.anc_x, xprev, (int)i);
     const double d = z - xk;
     acc.s[0] += d * d;
@@ -471,7 +471,7 @@ struct OpP2 {
     }
     v.yblk[r] = in.blk + z;
     ynew[r] = z;
-    peer_put(v.cm, ynew, r, z);  // the next P1 gathers y on every rank
+    peer_put_halo(v.cm, 1, ynew, r, r + v.yoff, z);  // the next P1 gathers y on every rank
   }
   __device__ void row(int r, double s, RedVals<0, 0> &acc) const { row_in(r, s, load_row(r), acc); }
   __device__ void finalize(const RedVals<0, 0> &) const {
@@ -1071,7 +1071,12 @@ struct OpPush {
       default: p = pick3(v.xs, ct->xcur); break;
     }
   }
-  __device__ void elem(int64_t i, RedVals<0, 0> &) const { peer_put(v.cm, p, i, p[i]); }
+  int full;  // replicate everything (vectors read back by the host), else the gather halos
+  int side;  // 0: x side, 1: y side
+  __device__ void elem(int64_t i, RedVals<0, 0> &) const {
+    if (full) peer_put(v.cm, p, i, p[i]);
+    else peer_put_halo(v.cm, side, p, i, i + (side ? v.yoff : v.xoff), p[i]);
+  }
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
 enum PushBuf : int { PB_Y = 0, PB_XEVAL, PB_DY0, PB_DY1, PB_DX0, PB_DX1, PB_PW, PB_TM, PB_RS, PB_X };
@@ -1770,13 +1775,15 @@ int pull_ctrl(aqp_solver *s) {
 
 // row shards: replicate this rank's slice of buffer `which` (PushBuf) into
 // the peers' copies and wait until every rank has done the same
-int push_buf(aqp_solver *s, int which) {
+int push_buf(aqp_solver *s, int which, bool full = false) {
   if (!s->shard) return AQP_OK;
   cudaStream_t st = s->p->ctx->stream;
   const bool yside = which == PB_Y || which == PB_DY0 || which == PB_DY1 || which == PB_TM;
   OpPush o{};
   o.v = s->v;
   o.which = which;
+  o.full = full ? 1 : 0;
+  o.side = yside ? 1 : 0;
   AQP_CUDA(run_elem(st, yside ? s->v.ml : s->v.nl, o, s->gr));
   k_comm_barrier<<<1, 32, 0, st>>>(s->gr);
   AQP_CUDA(cudaGetLastError());
@@ -1866,6 +1873,12 @@ int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, si
   }
   s->gr.comm.rank = p->rank;
   s->gr.comm.nranks = 1;  // until aqp_solver_connect
+  for (int k = 0; k < kMaxRanks; ++k) {
+    s->gr.comm.xlo[k] = 0;
+    s->gr.comm.xhi[k] = p->n;
+    s->gr.comm.ylo[k] = 0;
+    s->gr.comm.yhi[k] = p->m;
+  }
   v.cm = s->gr.comm;
   std::memset(&s->h, 0, sizeof(Ctrl));
   s->h.xcur = 0; s->h.xprev = 1; s->h.ycur = 0; s->h.yprev = 1;
@@ -1929,6 +1942,22 @@ int aqp_solver_exchange_region(aqp_solver *s, void **base, size_t *bytes) {
   if (!s || !base || !bytes) return fail(AQP_EINVAL, "NULL argument");
   *base = s->ws_base;
   *bytes = (size_t)((char *)s->gr.comm.cb - (char *)s->ws_base) + sizeof(CommBlock);
+  return AQP_OK;
+}
+
+int aqp_solver_set_halos(aqp_solver *s, const int64_t *x_lohi, const int64_t *y_lohi, int nranks) {
+  if (!s || !x_lohi || !y_lohi) return fail(AQP_EINVAL, "NULL argument");
+  if (nranks != s->p->nranks || nranks > kMaxRanks) return fail(AQP_EINVAL, "nranks differs from the problem's shard");
+  if (s->exec) return fail(AQP_ESTATE, "set the halos before aqp_solver_connect");
+  for (int k = 0; k < nranks; ++k) {
+    if (x_lohi[2 * k] < 0 || x_lohi[2 * k + 1] > s->p->n || y_lohi[2 * k] < 0 || y_lohi[2 * k + 1] > s->p->m)
+      return fail(AQP_EINVAL, "halo range outside [0,n) / [0,m)");
+    s->gr.comm.xlo[k] = x_lohi[2 * k];
+    s->gr.comm.xhi[k] = x_lohi[2 * k + 1];
+    s->gr.comm.ylo[k] = y_lohi[2 * k];
+    s->gr.comm.yhi[k] = y_lohi[2 * k + 1];
+  }
+  s->v.cm = s->gr.comm;
   return AQP_OK;
 }
 
@@ -2238,7 +2267,7 @@ int aqp_solver_read(aqp_solver *s, int which, double *host_out, int64_t len) {
   if (s->shard) {
     // collective: every rank replicates its slice, then reads the full vector
     static const int kPush[8] = {PB_XEVAL, PB_Y, PB_RS, PB_DY0, PB_DY1, PB_DX0, PB_DX1, PB_X};
-    AQP_TRY(push_buf(s, kPush[which]));
+    AQP_TRY(push_buf(s, kPush[which], true));
   }
   src -= yside ? v.yoff : v.xoff;
   cudaStream_t st = s->p->ctx->stream;

@@ -260,6 +260,14 @@ class DeviceSolver:
         nat.check(self.lib.aqp_solver_exchange_region(self.handle, C.byref(base), C.byref(nbytes)))
         return int(base.value), int(nbytes.value)
 
+    def set_halos(self, x_ranges, y_ranges):
+        """Per-rank gather ranges [lo, hi) for the x and y sides (aqp_solver_set_halos)."""
+        xr = np.ascontiguousarray(np.asarray(x_ranges, dtype=np.int64).reshape(-1))
+        yr = np.ascontiguousarray(np.asarray(y_ranges, dtype=np.int64).reshape(-1))
+        nat.check(self.lib.aqp_solver_set_halos(self.handle, xr.ctypes.data_as(nat.c_int64_p),
+                                                yr.ctypes.data_as(nat.c_int64_p), len(xr) // 2),
+                  "aqp_solver_set_halos")
+
     def connect(self, peer_bases):
         """Bind the peers' workspace mappings (index = rank) and build the graph."""
         arr = (C.c_void_p * len(peer_bases))(*[C.c_void_p(int(b)) for b in peer_bases])

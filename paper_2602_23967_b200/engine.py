@@ -209,6 +209,7 @@ class _Run:
             tol_scale=ip.scale, tol_floor=ip.floor, diag_bound=problem.quad.diag_bound(),
             adaptive=ip.adaptive, max_inner=ip.max_inner, halpern=params.halpern)
         if group is not None:
+            self.solver.problem_host = problem  # for the gather halos (shard.halos)
             group.connect(self.solver)
 
     def report(self, cr, need_slack: bool) -> ResidualReport:

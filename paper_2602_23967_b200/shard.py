@@ -84,6 +84,50 @@ def partition(problem, nranks: int) -> List[Rows]:
     return [(cx[k], cx[k + 1], cy[k], cy[k + 1]) for k in range(nranks)]
 
 
+def halos(problem, parts: Sequence[Rows]):
+    """Gather halos per rank: rank k gathers x only at the columns of its rows
+    of A and of the full symmetric Q, and y only at the columns of its rows of
+    A' (= the rows of A having a nonzero in its columns).  Returns two lists of
+    [lo, hi) ranges (global indices; empty ranges as (0, 0))."""
+    a = problem.constraint_matrix
+    n, m = problem.n, problem.m
+    ip, ix = np.asarray(a.indptr), np.asarray(a.indices)
+    arow = np.repeat(np.arange(m), np.diff(ip))
+    q = problem.quad
+    if q.kind == "sparse":
+        up = q.upper
+        qp, qi = np.asarray(up.indptr), np.asarray(up.indices)
+        qrow = np.repeat(np.arange(n), np.diff(qp))
+    xr, yr = [], []
+    for n0, n1, m0, m1 in parts:
+        lo, hi = n, 0
+        cols = ix[ip[m0]:ip[m1]]                      # A rows [m0, m1)
+        if cols.size:
+            lo, hi = min(lo, int(cols.min())), max(hi, int(cols.max()) + 1)
+        if q.kind == "sparse":
+            ucols = qi[qp[n0]:qp[n1]]                  # upper rows [n0, n1): j >= i
+            if ucols.size:
+                lo, hi = min(lo, int(ucols.min())), max(hi, int(ucols.max()) + 1)
+            sel = (qi >= n0) & (qi < n1)               # mirrored lower part: rows j < i
+            if sel.any():
+                r = qrow[sel]
+                lo, hi = min(lo, int(r.min())), max(hi, int(r.max()) + 1)
+        xr.append((lo, hi) if hi > lo else (0, 0))
+        sel = (ix >= n0) & (ix < n1)                   # A' rows [n0, n1) = A's columns
+        if sel.any():
+            r = arow[sel]
+            yr.append((int(r.min()), int(r.max()) + 1))
+        else:
+            yr.append((0, 0))
+    return xr, yr
+
+
+def _set_halos(solver, problem, nranks):
+    parts = partition(problem, nranks)
+    xr, yr = halos(problem, parts)
+    solver.set_halos(xr, yr)
+
+
 _Handle = C.c_char * 64  # cudaIpcMemHandle_t
 
 
@@ -138,6 +182,8 @@ class DistGroup(PeerGroup):
             self._mapped.append((int(ptr.value), o))
             bases.append(int(ptr.value))
         self.dist.barrier(group=self.group)  # every rank's mailbox is zero before anyone writes
+        if getattr(solver, "problem_host", None) is not None:
+            _set_halos(solver, solver.problem_host, self.nranks)
         solver.connect(bases)
         self.dist.barrier(group=self.group)
 
@@ -182,6 +228,8 @@ class LocalGroup(PeerGroup):
         base, _ = solver.exchange_region()
         self.shared.bases[self.rank] = base
         self.shared.barrier.wait()  # all created (mailboxes zeroed) and published
+        if getattr(solver, "problem_host", None) is not None:
+            _set_halos(solver, solver.problem_host, self.nranks)
         solver.connect(list(self.shared.bases))
         # graph instantiation may synchronise the device: no rank may start
         # exchanging (spinning) while another rank still builds its graph
@@ -256,4 +304,4 @@ def rows_of(problem, group: PeerGroup) -> Rows:
     return partition(problem, group.nranks)[group.rank]
 
 
-__all__ = ["partition", "PeerGroup", "DistGroup", "LocalGroup", "solve_local", "rows_of"]
+__all__ = ["partition", "halos", "PeerGroup", "DistGroup", "LocalGroup", "solve_local", "rows_of"]

@@ -103,3 +103,34 @@ def test_dist_group_gloo_world2():
     assert a0 == a1 == [True, False]
     p = instances.build("c1:1")
     assert [rows0, rows1] == shard.partition(p, 2)
+
+
+@pytest.mark.parametrize("spec", ["c5:5e3:50:0", "c1:0", "rqp:500:300:diagonal:0.02:5", "c2:1e4:5e3:0"])
+@pytest.mark.parametrize("nranks", [2, 5])
+def test_halos_cover_every_gathered_column(spec, nranks):
+    p = instances.build(spec)
+    parts = shard.partition(p, nranks)
+    xr, yr = shard.halos(p, parts)
+    a = p.constraint_matrix.to_scipy().tocsr()
+    at = a.T.tocsr()
+    q = p.quad
+    qf = None
+    if q.kind == "sparse":
+        u = q.upper.to_scipy()
+        qf = (u + u.T).tocsr()
+    for (n0, n1, m0, m1), (xl, xh), (yl, yh) in zip(parts, xr, yr):
+        cols = [a[m0:m1].indices]
+        if qf is not None:
+            cols.append(qf[n0:n1].indices)
+        c = np.concatenate(cols)
+        assert c.size == 0 or (c.min() >= xl and c.max() < xh)
+        r = at[n0:n1].indices
+        assert r.size == 0 or (r.min() >= yl and r.max() < yh)
+
+
+def test_banded_halos_are_strips():
+    p = instances.build("c5:5e4:500:0")
+    parts = shard.partition(p, 4)
+    xr, yr = shard.halos(p, parts)
+    for (n0, n1, m0, m1), (xl, xh) in zip(parts, xr):
+        assert n0 - xl <= 1000 and xh - n1 <= 1000  # Q band (i +- 1000) dominates A's +- 500
