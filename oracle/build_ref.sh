@@ -18,4 +18,6 @@ cp -r "$SRC" "$TMP/pkg"
 rm -rf "$HERE/_ref"
 python -m pip install --quiet --no-index --no-build-isolation --no-deps \
   --target "$HERE/_ref" "$TMP/pkg"
+# the reference's own tests, for oracle/ref_suite_plugin.py (git-ignored with the rest of _ref)
+cp -r "$TMP/pkg/tests" "$HERE/_ref/tests"
 PYTHONPATH="$HERE/_ref" python -c "import anchorqp; b = anchorqp.active_backend(); assert b == 'cython', b; print('oracle/_ref: anchorqp', anchorqp.__version__, 'backend', b)"
