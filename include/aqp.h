@@ -168,6 +168,15 @@ typedef struct {
   int64_t m0, m1;
 } aqp_shard;
 int aqp_problem_shard(aqp_problem *p, const aqp_shard *sh);
+
+/* Device-side Ruiz (ruiz_iters rounds of inf-norm equilibration of
+ * K = [[Q, A'], [A, 0]]) and optional Pock-Chambolle (alpha = 1, l1) scaling,
+ * applied IN PLACE to the device problem (A, A', Q, R, c, bounds).  D (n) and
+ * E (m) receive the scalings (device buffers); the solve of the scaled problem
+ * maps back by x = D x~, y = E y~.  Opt-in (not in the reference: the default
+ * solve never scales).  scratch: >= (2 n + m) doubles of device memory. */
+int aqp_problem_scale(aqp_problem *p, int ruiz_iters, int pock_chambolle, double *D, double *E, void *scratch,
+                      size_t scratch_bytes);
 int aqp_problem_destroy(aqp_problem *p);
 
 
@@ -229,6 +238,11 @@ int aqp_solver_sizes(const aqp_problem *p, size_t *workspace_bytes);
 int aqp_solver_create(aqp_problem *p, const aqp_solver_params *params, void *workspace,
                       size_t workspace_bytes, aqp_solver **out);
 int aqp_solver_destroy(aqp_solver *s);
+/* Scaled solves: dst (a solver of the ORIGINAL problem) <- the current
+ * iterate, anchor and window sums of src (a solver of the aqp_problem_scale'd
+ * problem) mapped back by x = D x~, y = E y~; then aqp_solver_check(dst, ...)
+ * certifies on the original problem.  Both solvers must share a stream. */
+int aqp_solver_import_scaled(aqp_solver *dst, aqp_solver *src, const double *D, const double *E);
 /* Row shards: the front of the solver workspace (every gathered vector and
  * the exchange mailbox) is written by the peers; its layout is identical on
  * every rank.  After every rank's aqp_solver_create has returned (host

@@ -126,6 +126,9 @@ SIGNATURES = {
     "aqp_solver_estimate_norm": (C.c_int, [_P, _P, C.c_int, c_double_p, C.POINTER(C.c_int)]),
     "aqp_solver_time_kernel": (C.c_int, [_P, C.c_int, C.c_int, _P, C.c_size_t, c_double_p]),
     "aqp_solver_trace": (C.c_int, [_P, _P, _I64, c_int64_p]),
+    # scaled solves (opt-in Ruiz / Pock-Chambolle)
+    "aqp_problem_scale": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P, C.c_size_t]),
+    "aqp_solver_import_scaled": (C.c_int, [_P, _P, _P, _P]),
     # row shards (multi-GPU)
     "aqp_problem_shard": (C.c_int, [_P, C.POINTER(Shard)]),
     "aqp_solver_exchange_region": (C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_size_t)]),

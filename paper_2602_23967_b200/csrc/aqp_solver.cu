@@ -1081,6 +1081,34 @@ struct OpPush {
 };
 enum PushBuf : int { PB_Y = 0, PB_XEVAL, PB_DY0, PB_DY1, PB_DX0, PB_DX1, PB_PW, PB_TM, PB_RS, PB_X };
 
+// ---------------------------------------------------------------- scaled solves
+// Certification of a scaled solve (aqp_problem_scale) on the ORIGINAL
+// problem: copy the scaled solver's current iterate, anchor and window sums
+// into an unscaled solver as x = D x~, y = E y~ (averages commute with the
+// diagonal map), which then runs the reference's checks unchanged.
+__global__ void __launch_bounds__(kThreads) k_import_scaled(SV dst, SV src, const double *__restrict__ D,
+                                                            const double *__restrict__ E, int64_t n, int64_t m) {
+  const Ctrl *sc = src.ctrl;
+  const double *sx = pick3(src.xs, sc->xcur), *sy = pick3(src.ys, sc->ycur);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = D[i];
+    dst.xs[0][i] = d * sx[i];
+    dst.anc_x[i] = d * src.anc_x[i];
+    dst.xblk[i] = d * src.xblk[i];
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const double e = E[i];
+    dst.ys[0][i] = e * sy[i];
+    dst.anc_y[i] = e * src.anc_y[i];
+    dst.yblk[i] = e * src.yblk[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    Ctrl *dc = dst.ctrl;
+    dc->xcur = 0; dc->xprev = 1; dc->ycur = 0; dc->yprev = 1;
+    dc->s.block_len = sc->s.block_len;
+  }
+}
+
 // ---------------------------------------------------------------- power iteration ops
 struct OpPwNorm {  // sum of squares of xbb[idx] -> red[slot]
   static constexpr int NS = 1, NM = 0;
@@ -1935,6 +1963,19 @@ int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, si
     }
   }
   *out = s;
+  return AQP_OK;
+}
+
+int aqp_solver_import_scaled(aqp_solver *dst, aqp_solver *src, const double *D, const double *E) {
+  if (!dst || !src || !D || !E) return fail(AQP_EINVAL, "NULL argument");
+  if (dst->p->n != src->p->n || dst->p->m != src->p->m || dst->shard || src->shard)
+    return fail(AQP_EINVAL, "import needs two unsharded solvers of the same shape");
+  cudaStream_t st = dst->p->ctx->stream;
+  if (src->p->ctx->stream != st) AQP_CUDA(cudaStreamSynchronize(src->p->ctx->stream));
+  const int64_t big = std::max(dst->p->n, dst->p->m);
+  k_import_scaled<<<elem_grid(big), kThreads, 0, st>>>(dst->v, src->v, D, E, dst->p->n, dst->p->m);
+  AQP_CUDA(cudaGetLastError());
+  dst->h.xcur = 0; dst->h.xprev = 1; dst->h.ycur = 0; dst->h.yprev = 1;
   return AQP_OK;
 }
 

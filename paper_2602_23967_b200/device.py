@@ -135,6 +135,20 @@ class DeviceProblem:
         nat.check(lib.aqp_problem_get_info(h, C.byref(info)))
         self.info = info
 
+    def scale(self, ruiz_iters: int = 10, pock_chambolle: bool = False):
+        """Equilibrate this device problem in place (aqp_problem_scale); returns
+        the (D, E) scalings as device tensors (x = D x~, y = E y~)."""
+        torch = self.ctx.torch
+        dev = f"cuda:{self.ctx.device}"
+        D = torch.empty(max(self.n, 1), dtype=torch.float64, device=dev)
+        E = torch.empty(max(self.m, 1), dtype=torch.float64, device=dev)
+        scratch = torch.empty(2 * self.n + self.m + 1, dtype=torch.float64, device=dev)
+        nat.check(self.ctx.lib.aqp_problem_scale(self.handle, int(ruiz_iters), int(bool(pock_chambolle)),
+                                                 C.c_void_p(D.data_ptr()), C.c_void_p(E.data_ptr()),
+                                                 C.c_void_p(scratch.data_ptr()), scratch.numel() * 8),
+                  "aqp_problem_scale")
+        return D[: self.n], E[: self.m]
+
     def shard(self, rank: int, nranks: int, n0: int, n1: int, m0: int, m1: int):
         """Restrict this rank's passes to rows [n0,n1) of A'/Q and [m0,m1) of A
         (aqp_problem_shard)."""
@@ -252,6 +266,12 @@ class DeviceSolver:
         buf = (C.c_int64 * 3)()
         nat.check(self.lib.aqp_solver_counters(self.handle, buf))
         return bool(buf[2])
+
+    def import_scaled(self, src: "DeviceSolver", D, E):
+        """This (original-problem) solver <- src's iterate, anchor and window
+        sums mapped back from the scaled space (aqp_solver_import_scaled)."""
+        nat.check(self.lib.aqp_solver_import_scaled(self.handle, src.handle, C.c_void_p(D.data_ptr()),
+                                                    C.c_void_p(E.data_ptr())), "aqp_solver_import_scaled")
 
     # -- row shards -------------------------------------------------------------
     def exchange_region(self):

@@ -93,6 +93,12 @@ class SolverParams:
     gamma_sys: Optional[float] = None
     norm_iters: int = 100
     norm_seed: int = 0
+    # extension (not in the reference, off by default -- SURVEY.md §0): device-
+    # side equilibration before the solve, "ruiz" or "ruiz_pc" (Ruiz rounds,
+    # then one Pock-Chambolle l1 pass); termination and certificates stay on
+    # the original problem
+    scaling: Optional[str] = None
+    scaling_iters: int = 10
 
     def __post_init__(self):
         if self.eps_tol <= 0 or self.eps_inf <= 0:
@@ -105,6 +111,8 @@ class SolverParams:
             raise ValueError("iter_limit and check_every must be positive")
         if self.time_limit is not None and self.time_limit <= 0:
             raise ValueError("time_limit must be positive")
+        if self.scaling not in (None, "ruiz", "ruiz_pc") or self.scaling_iters < 0:
+            raise ValueError("scaling must be None, 'ruiz' or 'ruiz_pc' with scaling_iters >= 0")
 
 
 @dataclasses.dataclass(frozen=True)
@@ -195,6 +203,9 @@ class _Run:
         self.progress = progress
         ctx = DeviceContext.get(device)
         self.dev = DeviceProblem(problem, ctx)
+        self.scaling = getattr(params, "scaling", None)
+        if self.scaling is not None and group is not None:
+            raise ValueError("scaling is not available for row-sharded solves")
         if group is not None:  # row shard of a multi-GPU solve (shard.py)
             from .shard import rows_of
 
@@ -204,17 +215,67 @@ class _Run:
         self.con_scale = certify.finite_bound_scale(problem.con_bounds)
         self.cost_inf = certify.linf(problem.cost)
         ip = params.inner
+        diag_bound = problem.quad.diag_bound()
+        self.checker_dev = None
+        if self.scaling is not None:
+            # iterate on an equilibrated copy; certify on the original (checker)
+            self.checker_dev = self.dev
+            self.dev = DeviceProblem(problem, ctx)
+            self.D, self.E = self.dev.scale(getattr(params, "scaling_iters", 10), self.scaling == "ruiz_pc")
+            diag_bound = _scaled_diag_bound(problem.quad, self.D.cpu().numpy())
         self.solver = DeviceSolver(
             self.dev, eps_tol=params.eps_tol, eps_inf=params.eps_inf, gamma_sys=gamma,
-            tol_scale=ip.scale, tol_floor=ip.floor, diag_bound=problem.quad.diag_bound(),
+            tol_scale=ip.scale, tol_floor=ip.floor, diag_bound=diag_bound,
             adaptive=ip.adaptive, max_inner=ip.max_inner, halpern=params.halpern)
+        self.checker = self.solver
+        if self.checker_dev is not None:
+            self.checker = DeviceSolver(
+                self.checker_dev, eps_tol=params.eps_tol, eps_inf=params.eps_inf, gamma_sys=gamma,
+                tol_scale=ip.scale, tol_floor=ip.floor, diag_bound=problem.quad.diag_bound(),
+                adaptive=ip.adaptive, max_inner=ip.max_inner, halpern=params.halpern)
         if group is not None:
             self.solver.problem_host = problem  # for the gather halos (shard.halos)
             group.connect(self.solver)
 
     def report(self, cr, need_slack: bool) -> ResidualReport:
-        slack = self.solver.read(DeviceSolver.DUAL_SLACK) if need_slack else None
+        slack = self.checker.read(DeviceSolver.DUAL_SLACK) if need_slack else None
         return certify.report_from_check(cr, self.con_scale, self.cost_inf, slack)
+
+    # certification on the original problem (identity unless scaling is on)
+    def check(self, with_rays: bool):
+        if self.checker is self.solver:
+            return self.solver.check(with_rays)
+        self.checker.import_scaled(self.solver, self.D, self.E)
+        cr = self.checker.check(with_rays)
+        if with_rays:  # engine.py:443-453 on the iterating solver too: window restarts
+            self.solver.reset_window()
+            sc = self.solver.get_scalars()
+            sc.block_len, sc.have_avg_prev = 0, 1
+            self.solver.set_scalars(sc)
+        return cr
+
+    def mark_cert(self):
+        if self.checker is not self.solver:
+            self.checker.import_scaled(self.solver, self.D, self.E)
+        self.checker.mark_cert()
+
+    def forget_window(self):
+        """After a halted window (engine.py:407-417): no previous averages."""
+        if self.checker is not self.solver:
+            sc = self.checker.get_scalars()
+            sc.have_avg_prev, sc.block_len = 0, 0
+            self.checker.set_scalars(sc)
+
+
+def _scaled_diag_bound(quad, d: np.ndarray) -> float:
+    """QuadOperator.diag_bound() of D Q D (inner.py:102) for the scaled solve."""
+    d2 = d * d
+    if quad.kind == "diagonal":
+        return float((d2 * quad.values).max(initial=0.0))
+    if quad.kind == "sparse":
+        return float((d2 * quad.diag).max(initial=0.0))
+    rsq = np.bincount(quad.r.indices, weights=quad.r.data ** 2, minlength=quad.n)
+    return float((d2 * (quad.p.diag + rsq)).max(initial=0.0))
 
 
 def solve(problem, params: Optional[SolverParams] = None, progress: Optional[ProgressCallback] = None,
@@ -247,17 +308,17 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
     n_outer = n_inner = restarts = 0
 
     def finish(status, report, cert):
-        x = sol.read(DeviceSolver.X_EVAL)
-        y = sol.read(DeviceSolver.Y)
+        x = run.checker.read(DeviceSolver.X_EVAL)
+        y = run.checker.read(DeviceSolver.Y)
         if report.dual_slack is None:
-            report = dataclasses.replace(report, dual_slack=sol.read(DeviceSolver.DUAL_SLACK))
+            report = dataclasses.replace(report, dual_slack=run.checker.read(DeviceSolver.DUAL_SLACK))
         return SolveResult(status=status, x=x, y=y, report=report, certificate=cert,
                            outer_iterations=n_outer, inner_iterations=n_inner, restarts=restarts,
                            seconds=time.monotonic() - start)
 
     # sharded: reading the slack is collective, so every rank reads it
     want_slack = progress is not None or group is not None
-    cr = sol.check(with_rays=False)
+    cr = run.check(with_rays=False)
     report = run.report(cr, want_slack)
     rs.best_residual_round_start = report.kkt_max
     rs.last_check_kkt = report.kkt_max
@@ -265,7 +326,7 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
         progress(0, report, rs.omega, rs.round)
     if certify.check_optimal(report, params.eps_tol):
         return finish(SolveStatus.OPTIMAL, report, None)
-    sol.mark_cert()
+    run.mark_cert()
     best_kkt_seen = report.kkt_max
     stall_checks = 0
     probe_until = 0
@@ -313,16 +374,17 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
             rs.round += 1
             rs.theta = rs.theta / 2.0 if rs.theta >= THETA_BACKOFF_FLOOR else 0.0
             rs.last_check_kkt = rs.best_residual_round_start
-            sol.mark_cert()
+            run.mark_cert()
             probe_until = 0
             sol.reset_window()
+            run.forget_window()
             push(k=0, theta=rs.theta, halted=0, block_len=0, have_avg_prev=0)
             continue
         at_cap = (not probing) and rp.enabled and sc.k >= rp.max_round_len
         if not (n_outer % check_every == 0 or at_cap or n_outer == params.iter_limit):
             continue  # window ended at the probe boundary
         # ---- certification point (engine.py:436-494) -----------------------
-        cr = sol.check(with_rays=True)
+        cr = run.check(with_rays=True)
         if monitor is not None:
             monitor(n_outer, n_inner)
         report = run.report(cr, want_slack)
@@ -335,16 +397,16 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
         for j in order:
             hit = certify.primal_ray_test(cr, j, params.eps_inf)
             if hit is not None:
-                ray = sol.read(DeviceSolver.YRAY0 + j)
+                ray = run.checker.read(DeviceSolver.YRAY0 + j)
                 return finish(SolveStatus.PRIMAL_INFEASIBLE, report,
                               Certificate(CertificateKind.PRIMAL_RAY, ray, hit[0], hit[1]))
         for j in order:
             hit = certify.dual_ray_test(cr, j, params.eps_tol, params.eps_inf, run.gamma_sys)
             if hit is not None:
-                ray = sol.read(DeviceSolver.XRAY0 + j)
+                ray = run.checker.read(DeviceSolver.XRAY0 + j)
                 return finish(SolveStatus.DUAL_INFEASIBLE, report,
                               Certificate(CertificateKind.DUAL_RAY, ray, hit[0], hit[1]))
-        sol.mark_cert()
+        run.mark_cert()
         if math.isfinite(kkt) and kkt < STALL_IMPROVEMENT * best_kkt_seen:
             best_kkt_seen = min(best_kkt_seen, kkt)
             stall_checks = 0
@@ -362,7 +424,7 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
             probe_until = n_outer + rp.max_round_len
         elif not math.isfinite(kkt) or kkt > DIVERGENCE_FACTOR * rs.best_residual_round_start:
             rollback_round()
-            sol.mark_cert()
+            run.mark_cert()
         elif rp.enabled and restart_decision(k_now, rs, kkt, params):
             if kkt < rs.best_residual_round_start:  # anti-windup, engine.py:284-290
                 rs.omega = pid_update(rs, math.sqrt(cr.pid_dx2), math.sqrt(cr.pid_dy2), params)
@@ -378,5 +440,5 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
             if out_of_time:
                 return finish(SolveStatus.TIME_LIMIT, report, None)
 
-    cr = sol.check(with_rays=False)
+    cr = run.check(with_rays=False)
     return finish(SolveStatus.ITERATION_LIMIT, run.report(cr, False), None)

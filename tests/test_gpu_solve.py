@@ -265,3 +265,23 @@ def test_persistent_window_kernel_is_bitwise_identical(cuda, spec, monkeypatch):
     b = solve(p, prm)
     assert (a.status, a.outer_iterations, a.inner_iterations) == (b.status, b.outer_iterations, b.inner_iterations)
     assert np.array_equal(a.x, b.x) and np.array_equal(a.y, b.y)
+
+
+@pytest.mark.parametrize("scaling", ["ruiz", "ruiz_pc"])
+@pytest.mark.parametrize("spec,fname", [("c1:0", "ref_c1_s0.json"),
+                                        ("rqp:300:150:low_rank:0.05:3", "ref_rqp_300_150_low_rank_0.05_3.json"),
+                                        ("rqp:500:300:diagonal:0.02:5", "ref_rqp_500_300_diagonal_0.02_5.json"),
+                                        ("c4i:1e3:1", "ref_c4i_1e3_1.json"), ("c4u:1e3:1", "ref_c4u_1e3_1.json")])
+def test_opt_in_scaling_keeps_status_and_objective(cuda, spec, fname, scaling):
+    """SolverParams(scaling=...) (extension, off by default): device-side
+    Ruiz / Pock-Chambolle equilibration; certification stays on the original
+    problem, so status and objective match the reference (iteration counts
+    differ by design)."""
+    g = golden(fname)
+    res = solve(instances.build(spec), SolverParams(eps_tol=g["eps_tol"], scaling=scaling))
+    assert res.status.value == g["status"]
+    if g["status"] == "optimal":
+        assert res.report.kkt_max <= g["eps_tol"]
+        assert abs(res.report.primal_objective - g["objective"]) <= 1e-6 * max(1.0, abs(g["objective"]))
+    else:
+        assert res.certificate is not None
