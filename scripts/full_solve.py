@@ -10,16 +10,17 @@ from bench_configs import build
 
 name = sys.argv[1]
 tl = float(sys.argv[2]) if len(sys.argv) > 2 else 1200.0
+scaling = sys.argv[3] if len(sys.argv) > 3 else None
 t = time.time()
 p = build(name)
 gen = time.time() - t
 trace = []
 t = time.time()
-res = aq.solve(p, aq.SolverParams(eps_tol=1e-8, time_limit=tl),
+res = aq.solve(p, aq.SolverParams(eps_tol=1e-8, time_limit=tl, scaling=scaling),
                progress=lambda k, rep, om, rd: trace.append((k, rep.kkt_max, om)))
 torch.cuda.synchronize()
 wall = time.time() - t
-print(json.dumps({"config": name, "n": p.n, "m": p.m, "status": res.status.value, "outer": res.outer_iterations,
+print(json.dumps({"config": name, "scaling": scaling, "n": p.n, "m": p.m, "status": res.status.value, "outer": res.outer_iterations,
                   "inner": res.inner_iterations, "restarts": res.restarts, "kkt": res.report.kkt_max,
                   "objective": res.report.primal_objective, "solve_s": round(wall, 2), "gen_s": round(gen, 1),
                   "outer_per_s": round(res.outer_iterations / wall, 1),
