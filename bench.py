@@ -142,6 +142,19 @@ def problem_bytes(p) -> int:
     return int(sum(x.nbytes for x in arrs))
 
 
+def host_cpu() -> dict:
+    """nproc and the CPU model of the box the reference timing ran on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
 def cpu_baseline(spec: str, warmup: int, steps: int, threads: int):
     env = dict(os.environ)
     if threads == 1:
@@ -173,7 +186,7 @@ def run_reference(args, world, rank):
                    "step": "one outer PDHG iteration (BB inner solve included) of the reference CPU solver",
                    "eps_tol": EPS},
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "inner_iters/s", "cores": threads, "kind": r["kind"],
+        "cpu_baseline": {"value": value, "unit": "inner_iters/s", "cores": threads, "kind": r["kind"], **host_cpu(),
                          "sample": f"outer iterations {max(args.warmup,1)}..{max(args.warmup,1)+args.steps} of the C2 solve "
                                    f"({r['inner']} BB iterations in {r['seconds']:.1f}s; backend {r['backend']})"},
         "e2e": {"value": value, "unit": "inner_iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -324,7 +337,7 @@ def run_ours(args, world, rank, local):
         try:
             cb = cpu_baseline(f"c2:{SPEC_N}:{SPEC_M}:0", 2, 8, threads=1)
             line["cpu_baseline"] = {"value": cb["inner"] / cb["seconds"], "unit": "inner_iters/s", "cores": 1,
-                                    "kind": cb["kind"],
+                                    "kind": cb["kind"], **host_cpu(),
                                     "sample": f"outer iterations 2..10 of the same C2 solve ({cb['inner']} BB "
                                               f"iterations in {cb['seconds']:.1f}s, backend {cb['backend']})"}
         except Exception as exc:  # reported, not fatal
