@@ -181,6 +181,78 @@ __device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *
 // UNIFORM: the plan is all THREAD items over [256 b, 256 b + 256) (the common
 // case of short-row matrices, e.g. every C2 pass); the instantiation then
 // carries only the thread-per-row path, which needs far fewer registers
+#ifndef AQP_VEC_STAGE
+#define AQP_VEC_STAGE 1
+#endif
+// Stage the products of one tile [k0, k1) (<= kTileNnz nonzeros) into shared
+// memory (sprod, and scol for a symmetric row split).  AQP_VEC_STAGE: 128-bit
+// loads -- one int4 of column indices and two double2 of values per
+// 4-nonzero chunk -- over the 16-byte aligned body, scalar head and tail;
+// the same products land in the same slots (bitwise the scalar staging).
+template <class Op>
+__device__ __forceinline__ void stage_tile(const DevCsr &M, int k0, int k1, const Op &o, double *sprod, int *scol) {
+#if AQP_VEC_STAGE
+  const int a0 = min((k0 + 3) & ~3, k1), a1 = max(a0, k1 & ~3);
+  {  // head [k0, a0) on threads 0..2, tail [a1, k1) on threads 4..6
+    const int t = threadIdx.x;
+    int k = -1;
+    if (t < a0 - k0) k = k0 + t;
+    else if (t >= 4 && t - 4 < k1 - a1) k = a1 + (t - 4);
+    if (k >= 0) {
+      const int c = __ldg(M.idx + k);
+      sprod[k - k0] = __ldg(M.val + k) * o.gather(c);
+      if constexpr (Op::SYM) scol[k - k0] = c;
+    }
+  }
+  constexpr int VU = kTileNnz / (4 * kThreads);
+  const int nch = (a1 - a0) >> 2;
+  int4 ci[VU];
+  double2 va[VU], vb[VU];
+#pragma unroll
+  for (int v = 0; v < VU; ++v) {
+    const int ch = threadIdx.x + v * kThreads;
+    if (ch < nch) {
+      const int k = a0 + 4 * ch;
+      ci[v] = __ldg(reinterpret_cast<const int4 *>(M.idx + k));
+      va[v] = __ldg(reinterpret_cast<const double2 *>(M.val + k));
+      vb[v] = __ldg(reinterpret_cast<const double2 *>(M.val + k + 2));
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < VU; ++v) {
+    const int ch = threadIdx.x + v * kThreads;
+    if (ch < nch) {
+      const int j = a0 + 4 * ch - k0;
+      sprod[j] = va[v].x * o.gather(ci[v].x);
+      sprod[j + 1] = va[v].y * o.gather(ci[v].y);
+      sprod[j + 2] = vb[v].x * o.gather(ci[v].z);
+      sprod[j + 3] = vb[v].y * o.gather(ci[v].w);
+      if constexpr (Op::SYM) {
+        scol[j] = ci[v].x;
+        scol[j + 1] = ci[v].y;
+        scol[j + 2] = ci[v].z;
+        scol[j + 3] = ci[v].w;
+      }
+    }
+  }
+#else
+  int cs[kTileNnz / kThreads];
+#pragma unroll
+  for (int u = 0; u < kTileNnz / kThreads; ++u) {
+    const int k = k0 + threadIdx.x + u * kThreads;
+    cs[u] = k < k1 ? __ldg(M.idx + k) : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < kTileNnz / kThreads; ++u) {
+    const int k = k0 + threadIdx.x + u * kThreads;
+    if (k < k1) {
+      sprod[k - k0] = __ldg(M.val + k) * o.gather(cs[u]);
+      if constexpr (Op::SYM) scol[k - k0] = cs[u];
+    }
+  }
+#endif
+}
+
 // One plan item of an SpMV pass with op `o`: the block's rows are summed
 // (THREAD / STAGED / WARP / LONGSEQ / LONG, see the file header) and their
 // epilogue accumulates into `acc`.  Shared by spmv_op (one item per block) and
@@ -241,20 +313,7 @@ __device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, c
     // rows of medium length: stage the tile's products with coalesced loads,
     // then one warp per row (tree order, deterministic)
     const int k0 = it.k0, k1 = it.k1;
-    int cs[kTileNnz / kThreads];
-#pragma unroll
-    for (int u = 0; u < kTileNnz / kThreads; ++u) {
-      const int k = k0 + threadIdx.x + u * kThreads;
-      cs[u] = k < k1 ? __ldg(M.idx + k) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < kTileNnz / kThreads; ++u) {
-      const int k = k0 + threadIdx.x + u * kThreads;
-      if (k < k1) {
-        sprod[k - k0] = __ldg(M.val + k) * o.gather(cs[u]);
-        if constexpr (Op::SYM) scol[k - k0] = cs[u];
-      }
-    }
+    stage_tile(M, k0, k1, o, sprod, scol);
     __syncthreads();
     for (int r = it.row0 + warp; r < it.row1; r += kWarps) {
       const int b = __ldg(M.ptr + r) - k0, e = __ldg(M.ptr + r + 1) - k0;
@@ -283,24 +342,7 @@ __device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, c
       b = __ldg(M.ptr + r) - k0;
       e = __ldg(M.ptr + r + 1) - k0;
     }
-    constexpr int U = kTileNnz / kThreads;
-    int cs[U];
-    double vs[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = k0 + threadIdx.x + u * kThreads;
-      const bool in = k < k1;
-      cs[u] = in ? __ldg(M.idx + k) : 0;
-      vs[u] = in ? __ldg(M.val + k) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int k = k0 + threadIdx.x + u * kThreads;
-      if (k < k1) {
-        sprod[k - k0] = vs[u] * o.gather(cs[u]);
-        if constexpr (Op::SYM) scol[k - k0] = cs[u];
-      }
-    }
+    stage_tile(M, k0, k1, o, sprod, scol);
     __syncthreads();
     if (has) {
       const int rg = r + M.row_off;
