@@ -42,6 +42,12 @@ struct aqp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int sm_count = 148;
+  // pinned host staging shared by every solver of this (device, stream):
+  // allocated once (cudaMallocHost / cudaFreeHost synchronise the device, so
+  // they must not run per solve while other streams work), used in stream order
+  void *pinned = nullptr;
+  void *bounce = nullptr;
+  unsigned ring_i = 0;
 };
 
 struct aqp_problem {

@@ -457,6 +457,8 @@ int aqp_ctx_create(int device, void *stream, aqp_ctx **out) {
 }
 
 int aqp_ctx_destroy(aqp_ctx *ctx) {
+  if (ctx && ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx && ctx->bounce) cudaFreeHost(ctx->bounce);
   delete ctx;
   return AQP_OK;
 }

@@ -1455,9 +1455,8 @@ struct aqp_solver {
     Ctrl ring[32];                // host -> device scalar pushes (reused after a sync)
     unsigned long long err;       // exchange error word
     int flag;                     // eager-mode flag reads
-  } *pin = nullptr;
-  unsigned ring_i = 0;
-  double *bounce = nullptr;       // vector reads / start-vector upload
+  } *pin = nullptr;               // the context's (aqp_ctx::pinned)
+  double *bounce = nullptr;       // vector reads / start-vector upload (aqp_ctx::bounce)
   static constexpr size_t kBounce = 1 << 21;  // doubles (16 MB)
   bool shard = false;       // problem is row-sharded (nranks > 1): graph built at connect
   bool persist = false;     // windows run as one cooperative kernel (small problems)
@@ -1760,7 +1759,7 @@ int build_graph_any(aqp_solver *s) {
 int push_scalars(aqp_solver *s) {
   s->h.tau = s->h.s.eta / s->h.s.omega;    // engine.py:148-150
   s->h.sigma = s->h.s.eta * s->h.s.omega;  // engine.py:152-154
-  Ctrl *slot = &s->pin->ring[s->ring_i++ % 32];
+  Ctrl *slot = &s->pin->ring[s->p->ctx->ring_i++ % 32];
   std::memcpy(slot, &s->h, offsetof(Ctrl, xcur));
   AQP_CUDA(cudaMemcpyAsync(s->d_ctrl, slot, offsetof(Ctrl, xcur), cudaMemcpyHostToDevice, s->p->ctx->stream));
   return AQP_OK;
@@ -1769,7 +1768,7 @@ int push_scalars(aqp_solver *s) {
 template <class T>
 int poke(aqp_solver *s, T Ctrl::*field, T value) {
   s->h.*field = value;
-  Ctrl *slot = &s->pin->ring[s->ring_i++ % 32];
+  Ctrl *slot = &s->pin->ring[s->p->ctx->ring_i++ % 32];
   slot->*field = value;
   AQP_CUDA(cudaMemcpyAsync(&(s->d_ctrl->*field), &(slot->*field), sizeof(T), cudaMemcpyHostToDevice,
                            s->p->ctx->stream));
@@ -1780,7 +1779,7 @@ int poke(aqp_solver *s, T Ctrl::*field, T value) {
 int push_all(aqp_solver *s) {
   s->h.tau = s->h.s.eta / s->h.s.omega;
   s->h.sigma = s->h.s.eta * s->h.s.omega;
-  Ctrl *slot = &s->pin->ring[s->ring_i++ % 32];
+  Ctrl *slot = &s->pin->ring[s->p->ctx->ring_i++ % 32];
   *slot = s->h;
   AQP_CUDA(cudaMemcpyAsync(s->d_ctrl, slot, sizeof(Ctrl), cudaMemcpyHostToDevice, s->p->ctx->stream));
   AQP_CUDA(cudaStreamSynchronize(s->p->ctx->stream));
@@ -1887,8 +1886,12 @@ int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, si
   v.ml = p->m1 - p->m0;
   s->ws_base = ws;
   s->shard = p->nranks > 1;
-  AQP_CUDA(cudaMallocHost(&s->pin, sizeof(aqp_solver::Pinned)));
-  AQP_CUDA(cudaMallocHost(&s->bounce, aqp_solver::kBounce * 8));
+  if (!p->ctx->pinned) {
+    AQP_CUDA(cudaMallocHost(&p->ctx->pinned, sizeof(aqp_solver::Pinned)));
+    AQP_CUDA(cudaMallocHost(&p->ctx->bounce, aqp_solver::kBounce * 8));
+  }
+  s->pin = static_cast<aqp_solver::Pinned *>(p->ctx->pinned);
+  s->bounce = static_cast<double *>(p->ctx->bounce);
   if (p->n0 || p->m0) {
     for (int i = 0; i < 3; ++i) { v.xs[i] += v.xoff; v.ys[i] += v.yoff; v.xbb[i] += v.xoff; }
     for (int i = 0; i < 2; ++i) { v.gbb[i] += v.xoff; v.dx[i] += v.xoff; v.dy[i] += v.yoff; }
@@ -2053,8 +2056,6 @@ int aqp_solver_destroy(aqp_solver *s) {
   if (s->gr.trace_n) cudaFree(s->gr.trace_n);
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->graph) cudaGraphDestroy(s->graph);
-  if (s->pin) cudaFreeHost(s->pin);
-  if (s->bounce) cudaFreeHost(s->bounce);
   delete s;
   return AQP_OK;
 }
