@@ -367,6 +367,13 @@ struct DevCsr {
   int smem_bytes = 0;                  // dynamic shared memory per block (WARP items only)
   int uniform = 0;                     // every item is THREAD over rows [256 b, 256 b + 256)
   int row_off = 0;                     // global index of local row 0 (row shards of a symmetric Q)
+  // SELL-32 copy of a uniform (THREAD-only) plan's matrix: the k-th nonzero of
+  // row r sits at sell_off[r / 32] + 32 k + r % 32, so the warp's k-th loads
+  // (one row per lane) are coalesced -- one L1 wavefront for 32 indices
+  // instead of ~5 for the strided CSR rows.  Same nonzeros, same order per row.
+  const int64_t *sell_off = nullptr;
+  const int *sell_idx = nullptr;
+  const double *sell_val = nullptr;
 };
 
 }  // namespace aqp

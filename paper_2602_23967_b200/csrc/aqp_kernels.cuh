@@ -272,6 +272,30 @@ __device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, c
       const int b = __ldg(M.ptr + r), e = __ldg(M.ptr + r + 1);
       const int rg = r + M.row_off;  // global row (diagonal position of a symmetric shard)
       double lo = 0.0, up = 0.0;
+      if ((UNIFORM || M.uniform) && M.sell_idx) {
+        // SELL-32: the warp's k-th nonzeros are contiguous (coalesced loads)
+        const int len = e - b;
+        const int64_t base = __ldg(M.sell_off + (r >> 5)) + (r & 31);
+        for (int k = 0; k < len; k += AQP_GATHER_BATCH) {
+          int cc[AQP_GATHER_BATCH];
+          double pv[AQP_GATHER_BATCH];
+#pragma unroll
+          for (int u = 0; u < AQP_GATHER_BATCH; ++u) {
+            const bool in = k + u < len;
+            cc[u] = in ? __ldg(M.sell_idx + base + 32 * (k + u)) : 0;
+            pv[u] = in ? __ldg(M.sell_val + base + 32 * (k + u)) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < AQP_GATHER_BATCH; ++u)
+            if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);
+#pragma unroll
+          for (int u = 0; u < AQP_GATHER_BATCH; ++u) {
+            if (k + u < len) {
+              if (Op::SYM && cc[u] < rg) lo += pv[u]; else up += pv[u];
+            }
+          }
+        }
+      } else {
 #if AQP_GATHER_BATCH > 1
       // the row's nonzeros in chunks of AQP_GATHER_BATCH: all index/value
       // loads of a chunk, then all its gathers, then the sums in column
@@ -303,6 +327,7 @@ __device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, c
         if (Op::SYM && c < rg) lo += p; else up += p;
       }
 #endif
+      }
       const double val = Op::SYM ? lo + up : up;
       if constexpr (RowInOf<Op>::value && RowInLateOf<Op>::value) rin = o.load_row(r);
       if constexpr (RowInOf<Op>::value) o.row_in(r, val, rin, acc); else o.row(r, val, acc);

@@ -243,6 +243,65 @@ static int counts_to_ptr(int *counts, int rows, int *ptr_out, void *tmp, size_t 
   return AQP_OK;
 }
 
+// SELL-32 copy of a uniform plan's matrix (DevCsr::sell_*): library-owned
+// device memory, released by free_sell (problem destroy / re-plan).
+__global__ void k_fill_sell(const int *__restrict__ ptr, const int *__restrict__ idx, const double *__restrict__ val,
+                            int rows, const int64_t *__restrict__ off, int *sidx, double *sval) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int b = ptr[r], e = ptr[r + 1];
+  const int64_t base = off[r >> 5] + (r & 31);
+  for (int k = 0; k < e - b; ++k) {
+    sidx[base + 32 * k] = idx[b + k];
+    sval[base + 32 * k] = val[b + k];
+  }
+}
+
+// stream-ordered (cudaMallocAsync / cudaFreeAsync): no device-wide
+// synchronisation while other streams (concurrent solves) are working
+void free_sell(DevCsr &M, cudaStream_t st) {
+  if (M.sell_off) cudaFreeAsync(const_cast<int64_t *>(M.sell_off), st);
+  if (M.sell_idx) cudaFreeAsync(const_cast<int *>(M.sell_idx), st);
+  if (M.sell_val) cudaFreeAsync(const_cast<double *>(M.sell_val), st);
+  M.sell_off = nullptr;
+  M.sell_idx = nullptr;
+  M.sell_val = nullptr;
+}
+
+template <class P>
+static int build_sell(aqp_ctx *ctx, DevCsr &M, const P *hp) {
+  free_sell(M, ctx->stream);
+  const char *e = getenv("AQP_SELL");
+  if (e && e[0] == '0') return AQP_OK;
+  const int64_t nsl = ((int64_t)M.rows + 31) / 32;
+  std::vector<int64_t> off((size_t)nsl + 1);
+  int64_t total = 0;
+  for (int64_t s = 0; s < nsl; ++s) {
+    int64_t w = 0;
+    for (int64_t r = 32 * s; r < std::min<int64_t>(32 * s + 32, M.rows); ++r) w = std::max<int64_t>(w, (int64_t)(hp[r + 1] - hp[r]));
+    off[s] = total;
+    total += 32 * w;
+  }
+  off[nsl] = total;
+  const int64_t nnz = (int64_t)(hp[M.rows] - hp[0]);
+  if (total > 3 * nnz + 32 * nsl) return AQP_OK;  // too much padding: keep the CSR rows
+  int64_t *doff = nullptr;
+  int *sidx = nullptr;
+  double *sval = nullptr;
+  cudaStream_t st = ctx->stream;
+  AQP_CUDA(cudaMallocAsync(&doff, (nsl + 1) * sizeof(int64_t), st));
+  AQP_CUDA(cudaMallocAsync(&sidx, std::max<int64_t>(total, 1) * sizeof(int), st));
+  AQP_CUDA(cudaMallocAsync(&sval, std::max<int64_t>(total, 1) * sizeof(double), st));
+  AQP_CUDA(cudaMemcpyAsync(doff, off.data(), (nsl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  k_fill_sell<<<(M.rows + 255) / 256, 256, 0, ctx->stream>>>(M.ptr, M.idx, M.val, M.rows, doff, sidx, sval);
+  AQP_CUDA(cudaGetLastError());
+  M.sell_off = doff;
+  M.sell_idx = sidx;
+  M.sell_val = sval;
+  AQP_CUDA(cudaStreamSynchronize(st));  // `off` is a pageable local
+  return AQP_OK;
+}
+
 int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *host_ptr64, bool strict,
                 PlanItem *plan_dev, int64_t plan_cap, double *seg_part, unsigned *seg_ticket,
                 int64_t seg_cap, bool may_stage) {
@@ -277,6 +336,8 @@ int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *h
   M.nlongseg = nlong;
   M.seg_part = seg_part;
   M.seg_ticket = seg_ticket;
+  if (M.uniform && !strict) return host_ptr64 ? build_sell(ctx, M, host_ptr64) : build_sell(ctx, M, host_ptr32);
+  free_sell(M, ctx->stream);
   return AQP_OK;
 }
 
@@ -688,6 +749,8 @@ int aqp_problem_get_info(const aqp_problem *p, aqp_problem_info *out) {
 }
 
 int aqp_problem_destroy(aqp_problem *p) {
+  if (p)
+    for (DevCsr *M : {&p->A, &p->At, &p->Q, &p->R, &p->Rt}) free_sell(*M, p->ctx->stream);
   delete p;
   return AQP_OK;
 }
