@@ -54,6 +54,17 @@ __global__ void k_scale_csr(DevCsr M, const double *__restrict__ rs, const doubl
   for (int k = M.ptr[r]; k < M.ptr[r + 1]; ++k) val[k] = val[k] * s * cs[M.idx[k]];
 }
 
+// the SELL-32 copy of a uniform plan's matrix (DevCsr::sell_*) follows its CSR
+__global__ void k_scale_sell(DevCsr M, const double *__restrict__ rs, const double *__restrict__ cs) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= M.rows || !M.sell_val) return;
+  const int len = M.ptr[r + 1] - M.ptr[r];
+  const int64_t base = M.sell_off[r >> 5] + (r & 31);
+  double *sval = const_cast<double *>(M.sell_val);
+  const double s = rs[r];
+  for (int k = 0; k < len; ++k) sval[base + 32 * k] = sval[base + 32 * k] * s * cs[M.sell_idx[base + 32 * k]];
+}
+
 __global__ void k_scale_dense(double *__restrict__ R, int k, int64_t n, const double *__restrict__ cs) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)k * n) return;
@@ -122,10 +133,13 @@ int aqp_problem_scale(aqp_problem *p, int ruiz_iters, int pock_chambolle, double
     if (m) k_update<<<grid_of(m), 256, 0, st>>>(E, ny, nullptr, m, l1);
     AQP_CUDA(cudaGetLastError());
   }
-  // apply in place
+  // apply in place (CSR values, and the SELL copies of uniform plans)
   if (m) k_scale_csr<<<grid_of(m), 256, 0, st>>>(p->A, E, D, const_cast<double *>(p->A.val));
   if (n) k_scale_csr<<<grid_of(n), 256, 0, st>>>(p->At, D, E, const_cast<double *>(p->At.val));
   if (sparse_q && n) k_scale_csr<<<grid_of(n), 256, 0, st>>>(p->Q, D, D, const_cast<double *>(p->Q.val));
+  if (m && p->A.sell_val) k_scale_sell<<<grid_of(m), 256, 0, st>>>(p->A, E, D);
+  if (n && p->At.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->At, D, E);
+  if (sparse_q && n && p->Q.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->Q, D, D);
   if (lowrank) {
     if (p->r_dense) {
       k_scale_dense<<<grid_of((int64_t)p->R.rows * n), 256, 0, st>>>(const_cast<double *>(p->R.val), p->R.rows, n, D);
@@ -135,6 +149,8 @@ int aqp_problem_scale(aqp_problem *p, int ruiz_iters, int pock_chambolle, double
       k_fill<<<grid_of(std::max<int64_t>(p->R.rows, 1)), 256, 0, st>>>(nx1, std::max<int64_t>(p->R.rows, 1), 1.0);
       k_scale_csr<<<grid_of(p->R.rows), 256, 0, st>>>(p->R, nx1, D, const_cast<double *>(p->R.val));
       k_scale_csr<<<grid_of(n), 256, 0, st>>>(p->Rt, D, nx1, const_cast<double *>(p->Rt.val));
+      if (p->R.sell_val) k_scale_sell<<<grid_of(p->R.rows), 256, 0, st>>>(p->R, nx1, D);
+      if (p->Rt.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->Rt, D, nx1);
     }
   }
   if (n) k_scale_vec<<<grid_of(n), 256, 0, st>>>(p->c, p->qd, p->vlo, p->vhi, D, n);
