@@ -181,61 +181,13 @@ __device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *
 // UNIFORM: the plan is all THREAD items over [256 b, 256 b + 256) (the common
 // case of short-row matrices, e.g. every C2 pass); the instantiation then
 // carries only the thread-per-row path, which needs far fewer registers
-#ifndef AQP_VEC_STAGE
-#define AQP_VEC_STAGE 1
-#endif
 // Stage the products of one tile [k0, k1) (<= kTileNnz nonzeros) into shared
-// memory (sprod, and scol for a symmetric row split).  AQP_VEC_STAGE: 128-bit
-// loads -- one int4 of column indices and two double2 of values per
-// 4-nonzero chunk -- over the 16-byte aligned body, scalar head and tail;
-// the same products land in the same slots (bitwise the scalar staging).
+// memory (sprod, and scol for a symmetric row split): thread t takes nonzeros
+// t, t + 256, ..., so each warp-wide load and gather covers 32 consecutive
+// nonzeros.  (128-bit int4 / double2 staging was measured 10% slower on the C5
+// A' pass: a warp's gather then spans 4x the nonzeros, i.e. more cache lines.)
 template <class Op>
 __device__ __forceinline__ void stage_tile(const DevCsr &M, int k0, int k1, const Op &o, double *sprod, int *scol) {
-#if AQP_VEC_STAGE
-  const int a0 = min((k0 + 3) & ~3, k1), a1 = max(a0, k1 & ~3);
-  {  // head [k0, a0) on threads 0..2, tail [a1, k1) on threads 4..6
-    const int t = threadIdx.x;
-    int k = -1;
-    if (t < a0 - k0) k = k0 + t;
-    else if (t >= 4 && t - 4 < k1 - a1) k = a1 + (t - 4);
-    if (k >= 0) {
-      const int c = __ldg(M.idx + k);
-      sprod[k - k0] = __ldg(M.val + k) * o.gather(c);
-      if constexpr (Op::SYM) scol[k - k0] = c;
-    }
-  }
-  constexpr int VU = kTileNnz / (4 * kThreads);
-  const int nch = (a1 - a0) >> 2;
-  int4 ci[VU];
-  double2 va[VU], vb[VU];
-#pragma unroll
-  for (int v = 0; v < VU; ++v) {
-    const int ch = threadIdx.x + v * kThreads;
-    if (ch < nch) {
-      const int k = a0 + 4 * ch;
-      ci[v] = __ldg(reinterpret_cast<const int4 *>(M.idx + k));
-      va[v] = __ldg(reinterpret_cast<const double2 *>(M.val + k));
-      vb[v] = __ldg(reinterpret_cast<const double2 *>(M.val + k + 2));
-    }
-  }
-#pragma unroll
-  for (int v = 0; v < VU; ++v) {
-    const int ch = threadIdx.x + v * kThreads;
-    if (ch < nch) {
-      const int j = a0 + 4 * ch - k0;
-      sprod[j] = va[v].x * o.gather(ci[v].x);
-      sprod[j + 1] = va[v].y * o.gather(ci[v].y);
-      sprod[j + 2] = vb[v].x * o.gather(ci[v].z);
-      sprod[j + 3] = vb[v].y * o.gather(ci[v].w);
-      if constexpr (Op::SYM) {
-        scol[j] = ci[v].x;
-        scol[j + 1] = ci[v].y;
-        scol[j + 2] = ci[v].z;
-        scol[j + 3] = ci[v].w;
-      }
-    }
-  }
-#else
   int cs[kTileNnz / kThreads];
 #pragma unroll
   for (int u = 0; u < kTileNnz / kThreads; ++u) {
@@ -250,7 +202,6 @@ __device__ __forceinline__ void stage_tile(const DevCsr &M, int k0, int k1, cons
       if constexpr (Op::SYM) scol[k - k0] = cs[u];
     }
   }
-#endif
 }
 
 // One plan item of an SpMV pass with op `o`: the block's rows are summed
