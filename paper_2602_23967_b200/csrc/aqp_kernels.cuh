@@ -51,6 +51,9 @@
 #ifndef AQP_UNIFORM_MIN_BLOCKS
 #define AQP_UNIFORM_MIN_BLOCKS 4
 #endif
+#ifndef AQP_SPMV_MIN_BLOCKS
+#define AQP_SPMV_MIN_BLOCKS 4
+#endif
 
 namespace aqp {
 
@@ -314,7 +317,7 @@ __device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, c
     RowIn rin{};
     int b = 0, e = 0;
     if (has) {
-      if constexpr (RowInOf<Op>::value) rin = o.load_row(r);
+      if constexpr (RowInOf<Op>::value) rin = o.load_row(r);  // early: measured best for STAGED
       b = __ldg(M.ptr + r) - k0;
       e = __ldg(M.ptr + r + 1) - k0;
     }

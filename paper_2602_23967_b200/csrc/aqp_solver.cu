@@ -430,6 +430,10 @@ struct OpXPost {
 struct OpP2 {
   static constexpr int NS = 0, NM = 0;
   static constexpr bool SYM = false, FINAL = true, SPLIT = true;
+  // measured (scripts/p2_ab.sh): late epilogue loads at 6 blocks/SM take the
+  // C5 dual pass from 2.53 to 2.04 ms and cost C2 2 us (once per outer iteration)
+  static constexpr bool ROWIN_LATE = true;
+  static constexpr int UNIFORM_BLOCKS = 6;
   SV v;
   const double *y, *yprev;
   double *ynew;
