@@ -388,8 +388,37 @@ struct OpStep {
     xn[i] = x;
     peer_put_halo(v.cm, 0, xn, i, i + v.xoff, x);  // the next G pass gathers x_t on every rank
   }
+  // elements 2j, 2j+1 with 128-bit loads / store (no reduction, so the
+  // result is the scalar op's); needs 16-byte aligned slices (even xoff)
+  __device__ void elem2(int64_t j) const {
+    const int64_t i = 2 * j;
+    const double2 a = *reinterpret_cast<const double2 *>(xo + i), g = *reinterpret_cast<const double2 *>(go + i);
+    const double2 lo = *reinterpret_cast<const double2 *>(v.vlo + i), hi = *reinterpret_cast<const double2 *>(v.vhi + i);
+    double2 x;
+    x.x = clip(a.x - alpha * g.x, lo.x, hi.x);
+    x.y = clip(a.y - alpha * g.y, lo.y, hi.y);
+    *reinterpret_cast<double2 *>(xn + i) = x;
+    peer_put_halo(v.cm, 0, xn, i, i + v.xoff, x.x);
+    peer_put_halo(v.cm, 0, xn, i + 1, i + 1 + v.xoff, x.y);
+  }
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
+
+// the BB step over pairs (OpStep::elem2), scalar tail; grid = elem_grid(n / 2)
+__global__ void __launch_bounds__(kThreads) k_step2(int64_t n, OpStep op, GridRed g) {
+  pdl_wait();
+  trace_mark(g, 1);
+  if (op.skip()) return;
+  OpStep o = op;
+  o.prepare();
+  const int64_t half = n >> 1, stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t j = (int64_t)blockIdx.x * kThreads + threadIdx.x; j < half; j += stride) o.elem2(j);
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    RedVals<0, 0> none;
+    o.elem(n - 1, none);
+  }
+  pdl_trigger();
+}
 
 // X: primal epilogue after the BB solve (engine.py:222, 230-245, 404-428)
 struct OpXPost {
@@ -1625,6 +1654,16 @@ int dense_lowrank(aqp_solver *s, int src) {
   return AQP_OK;
 }
 
+// stream launch of the BB step (paired 128-bit kernel when the slice is aligned)
+int run_step(cudaStream_t st, const SV &v, const OpStep &o, GridRed gr) {
+  if ((v.xoff & 1) == 0)
+    k_step2<<<elem_grid(std::max<int64_t>(v.nl / 2, 1)), kThreads, 0, st>>>(v.nl, o, gr);
+  else
+    elem_op<OpStep><<<elem_grid(v.nl), kThreads, 0, st>>>(v.nl, o, gr);
+  AQP_CUDA(cudaGetLastError());
+  return AQP_OK;
+}
+
 int add_lowrank(aqp_solver *s, cudaGraph_t g, GNode &last, int src) {
   aqp_problem *p = s->p;
   if (p->r_dense) {
@@ -1717,7 +1756,10 @@ int build_graph(aqp_solver *s) {
       OpStep st{};
       st.v = v;
       st.cond = u > 0;
-      AQP_CUDA(node_elem(ib, il, v.nl, st, gr));
+      if ((v.xoff & 1) == 0)  // 16-byte aligned slices: the paired (128-bit) step
+        AQP_CUDA(add_node(ib, il, (unsigned)elem_grid(std::max<int64_t>(v.nl / 2, 1)), k_step2, v.nl, st, gr));
+      else
+        AQP_CUDA(node_elem(ib, il, v.nl, st, gr));
       if (s->shard) AQP_CUDA(node_barrier(ib, il, gr));
       if (lowrank) AQP_TRY(add_lowrank(s, ib, il, 1));
       OpGrad<false> gg{};
@@ -2135,7 +2177,7 @@ static int run_eager(aqp_solver *s, int64_t n_iters) {
         if (!cont) break;
         OpStep sp{};
         sp.v = v;
-        AQP_CUDA(run_elem(st, v.nl, sp, gr));
+        AQP_TRY(run_step(st, v, sp, gr));
         if (s->shard) {
           k_comm_barrier<<<1, 32, 0, st>>>(gr);
           AQP_CUDA(cudaGetLastError());
@@ -2445,7 +2487,7 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
       case 1: {
         OpStep o{};
         o.v = v;
-        AQP_CUDA(run_elem(st, v.nl, o, gr));
+        AQP_TRY(run_step(st, v, o, gr));
         break;
       }
       case 2: {
