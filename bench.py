@@ -50,6 +50,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SPEC_N, SPEC_M = 1_000_000, 500_000
+# test hooks only (scripts/bench_dist_try.sh): a smaller instance, an iteration
+# cap, the gloo backend and ranks sharing one device -- never used by the driver
+_TEST_N = int(os.environ.get("AQP_BENCH_TEST_N", "0"))
+_TEST_ITERS = int(os.environ.get("AQP_BENCH_TEST_ITERS", "0"))
 CHECK_EVERY = 64
 EPS = 1e-8
 METRIC = "BB(CG)-inner iterations/s, C2 solve to 1e-8 rel. KKT"
@@ -119,7 +123,7 @@ def dist_init():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("AQP_BENCH_TEST_BACKEND", "nccl"))
     return world, rank, local
 
 
@@ -203,10 +207,11 @@ def run_ours(args, world, rank, local):
     from paper_2602_23967_b200.device import DeviceContext, DeviceProblem, DeviceSolver
     from paper_2602_23967_b200 import _native as nat
 
+    local = local % torch.cuda.device_count()  # ranks > devices only in the one-box test hook
     torch.cuda.set_device(local)
     sharded = world > 1 and not args.replicas
     seed = 0 if sharded else rank
-    problem = generators.lasso_style_qp(SPEC_N, SPEC_M, seed=seed)
+    problem = generators.lasso_style_qp(_TEST_N or SPEC_N, (_TEST_N // 2) or SPEC_M, seed=seed)
     group = None
     if sharded:
         from paper_2602_23967_b200.shard import DistGroup
@@ -231,7 +236,8 @@ def run_ours(args, world, rank, local):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = aq.solve(problem, aq.SolverParams(eps_tol=EPS), device=local, monitor=monitor, group=group)
+    prm = aq.SolverParams(eps_tol=EPS, iter_limit=_TEST_ITERS) if _TEST_ITERS else aq.SolverParams(eps_tol=EPS)
+    res = aq.solve(problem, prm, device=local, monitor=monitor, group=group)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     clk = clocks.stop()
