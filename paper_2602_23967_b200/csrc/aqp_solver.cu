@@ -25,6 +25,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "aqp_common.cuh"
 #include "aqp_internal.h"
 #include "aqp_kernels.cuh"
@@ -1220,6 +1222,113 @@ __global__ void __launch_bounds__(kFinThreads) fin_ctrl_op(Op op, GridRed g, uns
 }
 
 
+// The same fold + finalize on a cluster of 8 CTAs x 128 threads.  Measured
+// on C2 the one-block fold spends ~4.2 us loading the 3907 x 7 partials
+// (219 KB): one SM's share of L2 bandwidth.  Here CTA c is virtual threads
+// [128 c, 128 c + 128) of that 1024-thread block -- same per-thread sums,
+// whole virtual warps, same xor trees -- and the warp totals go to CTA 0
+// through distributed shared memory, which adds them in warp order: bitwise
+// the one-block fold, with 8 SMs pulling the partials.
+constexpr int kFoldCtas = 8;
+constexpr int kFoldThreads = kFinThreads / kFoldCtas;
+
+template <class Op>
+__global__ void __cluster_dims__(kFoldCtas, 1, 1) __launch_bounds__(kFoldThreads)
+    fin_ctrl_cl(Op op, GridRed g, unsigned nb) {
+  namespace cg = cooperative_groups;
+  constexpr int NS = Op::NS, NM = Op::NM, NT = NS + NM;
+  constexpr int W = (int)(sizeof(Ctrl) / 8);
+  constexpr int NW = kFinThreads / 32;
+  __shared__ unsigned long long cbuf[W];
+  __shared__ double swarp[NW * (NT > 0 ? NT : 1)];
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned crank = cl.block_rank();
+  pdl_wait();
+  const bool shard = g.comm.nranks > 1;
+  if (!shard) pdl_trigger();
+  trace_mark(g, 2);
+  if (op.skip()) {  // the same control block for every CTA: all skip or none
+    pdl_trigger();
+    return;
+  }
+  Ctrl *gctrl = op.v.ctrl;
+  if (crank == 0) {
+    const unsigned long long *src = reinterpret_cast<const unsigned long long *>(gctrl);
+    for (int i = threadIdx.x; i < W; i += blockDim.x) cbuf[i] = __ldcg(src + i);
+  }
+  RedVals<NS, NM> a;
+  a.zero();
+  if constexpr (NT > 0) {
+    constexpr int U = 4;
+    const unsigned vt = crank * kFoldThreads + threadIdx.x;  // virtual thread of the 1024-thread fold
+    for (unsigned b0 = vt; b0 < nb; b0 += U * kFinThreads) {
+      double t[U][NT];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned b = b0 + u * kFinThreads;
+#pragma unroll
+        for (int i = 0; i < NT; ++i) t[u][i] = b < nb ? g.partials[(size_t)i * nb + b] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int i = 0; i < NS; ++i) a.s[i] += t[u][i];
+#pragma unroll
+        for (int i = 0; i < NM; ++i) a.m[i] = nanmax(a.m[i], t[u][NS + i]);
+      }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+      for (int i = 0; i < NS; ++i) a.s[i] += __shfl_xor_sync(0xffffffffu, a.s[i], off);
+#pragma unroll
+      for (int i = 0; i < NM; ++i) a.m[i] = nanmax(a.m[i], __shfl_xor_sync(0xffffffffu, a.m[i], off));
+    }
+    if (lane == 0) {
+      double *dst = cl.map_shared_rank(swarp, 0);
+      const int vw = (int)crank * (kFoldThreads / 32) + warp;
+#pragma unroll
+      for (int i = 0; i < NS; ++i) dst[vw * NT + i] = a.s[i];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) dst[vw * NT + NS + i] = a.m[i];
+    }
+  }
+  cl.sync();  // every CTA's warp totals are in CTA 0
+  if (crank != 0) return;
+  if constexpr (NT > 0) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int i = 0; i < NS; ++i) a.s[i] = swarp[i];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) a.m[i] = swarp[NS + i];
+      for (int w = 1; w < NW; ++w) {
+#pragma unroll
+        for (int i = 0; i < NS; ++i) a.s[i] += swarp[w * NT + i];
+#pragma unroll
+        for (int i = 0; i < NM; ++i) a.m[i] = nanmax(a.m[i], swarp[w * NT + NS + i]);
+      }
+    }
+  }
+  __syncthreads();
+  comm_allreduce<NS, NM>(a, g.comm);
+  if (shard) pdl_trigger();
+  trace_mark(g, 4);
+  Op o = op;
+  o.v.ctrl = reinterpret_cast<Ctrl *>(cbuf);
+  o.prepare();
+  if (threadIdx.x == 0) o.finalize(a);
+  trace_mark(g, 5);
+  __syncthreads();
+  unsigned long long *dstc = reinterpret_cast<unsigned long long *>(gctrl);
+  for (int i = threadIdx.x; i < W; i += blockDim.x) dstc[i] = cbuf[i];
+  trace_mark(g, 3);
+}
+
+#ifndef AQP_FOLD_CLUSTER
+#define AQP_FOLD_CLUSTER 1
+#endif
+
 // ================================================================ persistent window kernel
 // Small problems (C1, C4: a few thousand to 1e5 rows) spend their time in
 // launch latency, not bytes: a BB iteration is three dependent kernels of a
@@ -1598,13 +1707,23 @@ cudaError_t node_spmv_fin(cudaGraph_t g, GNode &last, const DevCsr &M, const Op 
                             : add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M,
                                             op, gr);
   if (e != cudaSuccess) return e;
+#if AQP_FOLD_CLUSTER
+  return add_node_cfg(g, last, (unsigned)kFoldCtas, (unsigned)kFoldThreads, 0u, fin_ctrl_cl<Op>, op, gr,
+                      (unsigned)M.nitems);
+#else
   return add_node_cfg(g, last, 1u, (unsigned)kFinThreads, 0u, fin_ctrl_op<Op>, op, gr, (unsigned)M.nitems);
+#endif
 }
 template <class Op>
 cudaError_t node_elem_fin(cudaGraph_t g, GNode &last, int64_t n, const Op &op, GridRed gr) {
   cudaError_t e = add_node(g, last, (unsigned)elem_grid(n), elem_op<Op>, n, op, gr);
   if (e != cudaSuccess) return e;
+#if AQP_FOLD_CLUSTER
+  return add_node_cfg(g, last, (unsigned)kFoldCtas, (unsigned)kFoldThreads, 0u, fin_ctrl_cl<Op>, op, gr,
+                      (unsigned)elem_grid(n));
+#else
   return add_node_cfg(g, last, 1u, (unsigned)kFinThreads, 0u, fin_ctrl_op<Op>, op, gr, (unsigned)elem_grid(n));
+#endif
 }
 
 // row shards: a one-block exchange after a producer whose output the next
@@ -1632,13 +1751,21 @@ cudaError_t run_spmv_fin(cudaStream_t st, const DevCsr &M, const Op &op, GridRed
     spmv_op<Op, true><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
   else
     spmv_op<Op><<<M.nitems, kThreads, M.smem_bytes, st>>>(M, op, gr);
+#if AQP_FOLD_CLUSTER
+  fin_ctrl_cl<Op><<<kFoldCtas, kFoldThreads, 0, st>>>(op, gr, (unsigned)M.nitems);
+#else
   fin_ctrl_op<Op><<<1, kFinThreads, 0, st>>>(op, gr, (unsigned)M.nitems);
+#endif
   return cudaGetLastError();
 }
 template <class Op>
 cudaError_t run_elem_fin(cudaStream_t st, int64_t n, const Op &op, GridRed gr) {
   elem_op<Op><<<elem_grid(n), kThreads, 0, st>>>(n, op, gr);
+#if AQP_FOLD_CLUSTER
+  fin_ctrl_cl<Op><<<kFoldCtas, kFoldThreads, 0, st>>>(op, gr, (unsigned)elem_grid(n));
+#else
   fin_ctrl_op<Op><<<1, kFinThreads, 0, st>>>(op, gr, (unsigned)elem_grid(n));
+#endif
   return cudaGetLastError();
 }
 
@@ -2480,7 +2607,11 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
       case 5: {
         OpGrad<false> o{};
         o.v = v;
+#if AQP_FOLD_CLUSTER
+        fin_ctrl_cl<OpGrad<false>><<<kFoldCtas, kFoldThreads, 0, st>>>(o, gr, (unsigned)p->Q.nitems);
+#else
         fin_ctrl_op<OpGrad<false>><<<1, kFinThreads, 0, st>>>(o, gr, (unsigned)p->Q.nitems);
+#endif
         AQP_CUDA(cudaGetLastError());
         break;
       }
