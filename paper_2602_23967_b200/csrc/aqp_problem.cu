@@ -314,7 +314,8 @@ int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *h
   // (P1, 2.80 -> 2.55 ms) but slows the A pass (P2, whose epilogue operands
   // are held across the staging barrier: 2.51 -> 2.86 ms), so only A' stages
   double staged_min = may_stage ? 8.0 : 1e300;
-  if (const char *e = getenv("AQP_STAGED_MIN")) staged_min = atof(e);
+  if (const char *e = getenv("AQP_STAGED_MIN"))  // A/B knob for the matrices that may stage (A')
+    if (may_stage) staged_min = atof(e);
   const int64_t nnz_rows = M.rows > 0 ? (host_ptr64 ? host_ptr64[M.rows] - host_ptr64[0]
                                                     : (int64_t)host_ptr32[M.rows] - host_ptr32[0]) : 0;
   const bool staged = !strict && M.rows > 0 && (double)nnz_rows >= staged_min * (double)M.rows;
