@@ -14,7 +14,7 @@ AQP_EAGER=1 $NCU -k 'regex:spmv_op<aqp::OpGrad<\(bool\)0>, \(bool\)1>' -s 20 -c 
     python scripts/prof_c2.py 64 > gpurun_out/ncu/c2.log 2>&1
 AQP_EAGER=1 $NCU -k 'regex:elem_op<aqp::OpStep' -s 20 -c 1 -o gpurun_out/ncu/c2_bb_step \
     python scripts/prof_c2.py 64 >> gpurun_out/ncu/c2.log 2>&1
-AQP_EAGER=1 $NCU -k 'regex:fin_ctrl_op<aqp::OpGrad<\(bool\)0>' -s 20 -c 1 -o gpurun_out/ncu/c2_bb_fold \
+AQP_EAGER=1 $NCU -k 'regex:fin_ctrl_(op|cl)<aqp::OpGrad<\(bool\)0>' -s 20 -c 1 -o gpurun_out/ncu/c2_bb_fold \
     python scripts/prof_c2.py 64 >> gpurun_out/ncu/c2.log 2>&1
 AQP_EAGER=1 $NCU -k 'regex:spmv_op<aqp::OpP1Bb' -s 2 -c 1 -o gpurun_out/ncu/c2_p1 \
     python scripts/prof_c2.py 64 >> gpurun_out/ncu/c2.log 2>&1
