@@ -374,6 +374,11 @@ struct DevCsr {
   const int64_t *sell_off = nullptr;
   const int *sell_idx = nullptr;
   const double *sell_val = nullptr;
+  // full symmetric Q of a uniform plan: its diagonal moved out of the CSR into
+  // diag[local row].  A row's upper sum starts with diag * x[row] -- the
+  // diagonal is the first j >= i entry, so the order is unchanged -- and the
+  // CSR loop is one nonzero (often one gather batch) shorter.
+  const double *diag = nullptr;
 };
 
 }  // namespace aqp

@@ -58,6 +58,7 @@ struct aqp_problem {
   aqp::DevCsr A, At, Q, R, Rt;
   int64_t q_full_nnz = 0;
   int r_dense = 0;  // R held dense row-major in R.val (R.rows x n); no R' CSR
+  double *qdiag = nullptr;  // Q's diagonal when split out of its CSR (DevCsr::diag)
   double *c = nullptr, *vlo = nullptr, *vhi = nullptr, *qd = nullptr, *clo = nullptr, *chi = nullptr;
   int8_t *cone_r = nullptr, *recc_x = nullptr, *cone_y = nullptr, *recc_s = nullptr;
   int *bad = nullptr;

@@ -226,6 +226,7 @@ __device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, c
       const int b = __ldg(M.ptr + r), e = __ldg(M.ptr + r + 1);
       const int rg = r + M.row_off;  // global row (diagonal position of a symmetric shard)
       double lo = 0.0, up = 0.0;
+      if (Op::SYM && M.diag) up = __ldg(M.diag + r) * o.gather(rg);  // split diagonal, first of the j >= i sum
       if ((UNIFORM || M.uniform) && M.sell_idx) {
         // SELL-32: the warp's k-th nonzeros are contiguous (coalesced loads)
         const int len = e - b;

@@ -305,6 +305,34 @@ static int build_sell(aqp_ctx *ctx, DevCsr &M, const P *hp) {
   return AQP_OK;
 }
 
+// ---------------------------------------------------------------- diagonal split (DevCsr::diag)
+__global__ void k_diag_pos(const int *__restrict__ ptr, const int *__restrict__ idx, int rows, int *missing) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  bool found = false;
+  for (int k = ptr[r]; k < ptr[r + 1]; ++k) found |= idx[k] == r;
+  if (!found) atomicAdd(missing, 1);
+}
+// row r loses exactly its diagonal entry: new ptr = old ptr - r
+__global__ void k_split_diag(const int *__restrict__ optr, const int *__restrict__ oidx,
+                             const double *__restrict__ oval, int rows, int *nptr, int *nidx, double *nval,
+                             double *diag) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > rows) return;
+  nptr[r] = optr[r] - r;
+  if (r == rows) return;
+  int w = optr[r] - r;
+  for (int k = optr[r]; k < optr[r + 1]; ++k) {
+    if (oidx[k] == r) {
+      diag[r] = oval[k];
+    } else {
+      nidx[w] = oidx[k];
+      nval[w] = oval[k];
+      ++w;
+    }
+  }
+}
+
 int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *host_ptr64, bool strict,
                 PlanItem *plan_dev, int64_t plan_cap, double *seg_part, unsigned *seg_ticket,
                 int64_t seg_cap, bool may_stage) {
@@ -539,11 +567,53 @@ static int check_desc(const aqp_problem_desc *d) {
   return AQP_OK;
 }
 
+// Move the diagonal of a uniform-plan full symmetric Q out of the CSR (every
+// row must hold one); scratch holds the old arrays during the compaction.
+static int split_q_diag(aqp_ctx *ctx, aqp_problem *p, Bump &scratch) {
+  DevCsr &M = p->Q;
+  const char *e = getenv("AQP_SPLIT_DIAG");
+  if ((e && e[0] == '0') || !M.uniform || M.rows == 0) return AQP_OK;
+  cudaStream_t st = ctx->stream;
+  const int n = M.rows;
+  const int64_t nnz = M.nnz;
+  scratch.used = 0;
+  int *missing = (int *)scratch.take(64);
+  int *oidx = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
+  double *oval = (double *)scratch.take(std::max<int64_t>(nnz, 1) * 8);
+  int *optr = (int *)scratch.take((int64_t)(n + 1) * 4);
+  if (scratch.overflow) return AQP_OK;  // not enough scratch: keep the diagonal in the CSR
+  AQP_CUDA(cudaMemsetAsync(missing, 0, 4, st));
+  k_diag_pos<<<(n + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, n, missing);
+  AQP_CUDA(cudaGetLastError());
+  int miss = 0;
+  AQP_CUDA(cudaMemcpyAsync(&miss, missing, 4, cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  if (miss) return AQP_OK;
+  CsrStore &s = p->sQ;
+  AQP_CUDA(cudaMemcpyAsync(oidx, M.idx, nnz * 4, cudaMemcpyDeviceToDevice, st));
+  AQP_CUDA(cudaMemcpyAsync(oval, M.val, nnz * 8, cudaMemcpyDeviceToDevice, st));
+  AQP_CUDA(cudaMemcpyAsync(optr, M.ptr, (int64_t)(n + 1) * 4, cudaMemcpyDeviceToDevice, st));
+  k_split_diag<<<(n + 256) / 256, 256, 0, st>>>(optr, oidx, oval, n, s.ptr, s.idx, s.val, p->qdiag);
+  AQP_CUDA(cudaGetLastError());
+  std::vector<int> hptr((size_t)n + 1);
+  AQP_CUDA(cudaMemcpyAsync(hptr.data(), s.ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  M.nnz = nnz - n;
+  M.diag = p->qdiag;
+  AQP_TRY(finish_plan(ctx, M, hptr.data(), nullptr, false, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap,
+                      false));
+  if (!M.uniform) return fail(AQP_ECUDA, "diagonal split changed the Q plan kind");
+  return AQP_OK;
+}
+
 static void layout_problem(Bump &b, const aqp_problem_desc *d, aqp_problem *p) {
   const int64_t n = d->n, m = d->m;
   layout_csr(b, p->sA, m, d->a_nnz);
   layout_csr(b, p->sAt, n, d->a_nnz);
-  if (d->quad_kind != AQP_QUAD_DIAGONAL) layout_csr(b, p->sQ, n, 2 * d->q_nnz);
+  if (d->quad_kind != AQP_QUAD_DIAGONAL) {
+    layout_csr(b, p->sQ, n, 2 * d->q_nnz);
+    p->qdiag = (double *)b.take(std::max<int64_t>(n, 1) * 8);
+  }
   if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
     if (d->r_dense) {
       p->sR.val = (double *)b.take(std::max<int64_t>(d->r_rows * n, 1) * 8);
@@ -653,6 +723,8 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
     rest.cap = scratch_bytes - ((ub.used + 255) & ~size_t(255));
     rc = symmetrize_csr(ctx, U, p->sQ, p->Q, false, rest, &p->q_full_nnz);
     if (rc) return cleanup(rc);
+    rc = split_q_diag(ctx, p, rest);
+    if (rc) return cleanup(rc);
     if (n) AQP_CUDA(cudaMemcpyAsync(p->qd, d->q_diag, n * 8, cudaMemcpyDeviceToDevice, st));
     if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && d->r_dense) {
       // full rows: the CSR values are R row-major; check the implied pattern
@@ -711,6 +783,7 @@ static int slice_rows(aqp_ctx *ctx, DevCsr &M, CsrStore &s, int64_t r0, int64_t 
   AQP_CUDA(cudaMemcpyAsync(hptr.data(), M.ptr + r0, hptr.size() * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   AQP_CUDA(cudaStreamSynchronize(ctx->stream));
   M.ptr += r0;
+  if (M.diag) M.diag += r0;
   M.rows = (int)(r1 - r0);
   M.nnz = (int64_t)hptr.back() - hptr.front();
   M.row_off = row_off;

@@ -92,6 +92,18 @@ __global__ void k_diag_norm(const double *__restrict__ q, const double *__restri
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = fabs(q[i]) * D[i] * D[i];
 }
+// a split-out diagonal of Q (DevCsr::diag) joins the row norm / is scaled by D^2
+__global__ void k_add_diag_norm(double *__restrict__ nrm, const double *__restrict__ q, const double *__restrict__ D,
+                                int64_t n, int l1) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = fabs(q[i]) * D[i] * D[i];
+  nrm[i] = l1 ? nrm[i] + v : fmax(nrm[i], v);
+}
+__global__ void k_scale_diag(double *q, const double *D, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) q[i] *= D[i] * D[i];
+}
 __global__ void k_fill(double *p, int64_t n, double v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -123,6 +135,7 @@ int aqp_problem_scale(aqp_problem *p, int ruiz_iters, int pock_chambolle, double
     if (n) k_row_norm<<<grid_of(n), 256, 0, st>>>(p->At, D, E, l1, nx1);
     if (sparse_q && n) {
       k_row_norm<<<grid_of(n), 256, 0, st>>>(p->Q, D, D, l1, nx2);  // full symmetric P: rows = columns
+      if (p->Q.diag) k_add_diag_norm<<<grid_of(n), 256, 0, st>>>(nx2, p->Q.diag, D, n, l1);
     } else if (n) {
       k_diag_norm<<<grid_of(n), 256, 0, st>>>(p->qd, D, n, nx2);    // diagonal Q: |q_j| d_j^2
     }
@@ -137,6 +150,7 @@ int aqp_problem_scale(aqp_problem *p, int ruiz_iters, int pock_chambolle, double
   if (m) k_scale_csr<<<grid_of(m), 256, 0, st>>>(p->A, E, D, const_cast<double *>(p->A.val));
   if (n) k_scale_csr<<<grid_of(n), 256, 0, st>>>(p->At, D, E, const_cast<double *>(p->At.val));
   if (sparse_q && n) k_scale_csr<<<grid_of(n), 256, 0, st>>>(p->Q, D, D, const_cast<double *>(p->Q.val));
+  if (sparse_q && n && p->Q.diag) k_scale_diag<<<grid_of(n), 256, 0, st>>>(const_cast<double *>(p->Q.diag), D, n);
   if (m && p->A.sell_val) k_scale_sell<<<grid_of(m), 256, 0, st>>>(p->A, E, D);
   if (n && p->At.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->At, D, E);
   if (sparse_q && n && p->Q.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->Q, D, D);
