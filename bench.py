@@ -1,42 +1,49 @@
-"""Benchmark of the PDHCG-II solve loop on BASELINE config 2 (C2).
+"""Benchmark of the PDHCG-II solve loop; headline on BASELINE config 5 (C5).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (N = 1): ``lasso_style_qp(n=1e6, m=5e5, seed)`` -- the Lasso-style
-sparse QP with Q = D + S (5e6 nnz full) and A (4e6 nnz) of BASELINE.json
-configs[1] -- solved to 1e-8 relative KKT through the public
-``paper_2602_23967_b200.solve`` from host (numpy) arrays.
+Headline workload (the largest config BASELINE.json runs on one GPU, and the
+one it row-partitions over 1/2/4/8 GPUs): **C5** = ``banded_qp(n=m=5e7,
+half_width=5000, seed=0)`` -- A with 5e8 nonzeros (10 per row, banded-local
+columns), Q = D + S with 2.5e8 nonzeros in its full symmetric form -- solved
+through the public ``paper_2602_23967_b200.solve`` from host (numpy) arrays
+with eps_tol = 1e-8 and the reference's default parameters.
 
-* A *step* is one certification window of that solve: 64 outer PDHG
-  iterations, each with its full BB inner solve, plus the certification point
-  (device residuals, ray tests, host branch logic).  W windows are warm-up,
-  the next K are timed with CUDA events on the solver stream (synchronised on
-  both sides by the certification point itself).
-* ``value`` = BB inner iterations / s over the K timed windows, summed over
-  ranks and divided by the max rank time ("CG-inner iters/s" of BASELINE.json;
-  the reference's inner solver is BB).
-* ``e2e`` = the same metric over the WHOLE solve call to 1e-8 from host
-  buffers: problem upload (H2D), A'/Q build, norm estimate, all iterations,
-  and the read-back of x, y (D2H) -- ``solve_time_s`` is that call's wall time.
-* ``roofline``: the dominant kernel (BB gradient pass: Q SpMV + gradient
-  epilogue + 7 reductions) timed stand-alone with an L2 flush before each
-  launch; algorithmic bytes per launch from SURVEY.md §8(d).
-* ``cpu_baseline``: the reference solver (oracle/_ref, Cython) on the host,
-  1 core, bounded sample of the same solve (rank 0, N = 1).
+* A *step* is one outer PDHG iteration of that solve, with its full BB inner
+  solve (A'y pass, BB iterations, x-bar, A x-bar pass, Halpern, window sums).
+  Outer iterations [0, W) are warm-up; [W, W+K) are timed with CUDA events on
+  the solver stream (the window graphs are split at W and W+K by
+  ``solve(..., marks=...)``; splitting does not change the trajectory).  The
+  reference arm times the SAME outer iterations [W, W+K) of the same solve of
+  the same instance, so both arms measure identical work.
+* ``value`` = BB inner iterations / s over the timed outer iterations
+  ("CG-inner iters/s" of BASELINE.json; the reference's inner solver is BB,
+  SURVEY.md §0), max-over-ranks device time.
+* ``e2e`` = the same metric over the WHOLE ``solve`` call (iter_limit = W+K)
+  from host buffers: problem upload (H2D), A'/Q build, norm estimate, the W+K
+  iterations, the final check and the read-back of x, y (D2H).
+* ``roofline``: the dominant kernel of a C5 outer iteration (the BB gradient
+  pass: Q SpMV + gradient epilogue + 7 reductions, run 1 + t times per outer
+  iteration) timed stand-alone; algorithmic bytes per launch from SURVEY.md
+  §8(d) (12 B/nnz + 4 B/row + 64 B/entry).
+* ``cpu_baseline``: the reference solver (oracle/_ref, Cython) in this
+  process on one core, one outer iteration of the same C5 solve (rank 0,
+  N = 1).
+* Secondary keys: ``c3_solve`` (config 3, n = 5e6 factor-model portfolio,
+  solved to 1e-8) and ``c2_solve`` (config 2, n = 1e6 Lasso-style QP, solved
+  to 1e-8), each a full solve timed end to end.
 
-N > 1 (torchrun): ONE C2 solve row-sharded over the N GPUs (SURVEY.md §8(e),
-paper_2602_23967_b200/shard.py): rank r owns a block of rows of A, A' and Q,
-the gathered vectors are replicated by NVLink peer stores and every
-reduction is a one-block mailbox exchange -- strong scaling of the same
-workload; ``value`` is that solve's BB iterations / s (max-over-ranks device
-time).  ``--replicas`` instead runs N independent C2 solves (weak scaling).
-``--impl reference`` times the reference CPU solver (rank 0 only) on the
-same workload and metric.
+N > 1 (torchrun): ONE C5 solve row-sharded over the N GPUs (SURVEY.md §8(e),
+paper_2602_23967_b200/shard.py) -- strong scaling of the same workload and
+step range; ``value`` is that solve's BB iterations / s over [W, W+K)
+(max-over-ranks device time).  ``--impl reference`` times the reference CPU
+solver (rank 0 only) on the same workload, range and metric.
 """
 
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -49,15 +56,27 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SPEC_N, SPEC_M = 1_000_000, 500_000
-# test hooks only (scripts/bench_dist_try.sh): a smaller instance, an iteration
-# cap, the gloo backend and ranks sharing one device -- never used by the driver
+C5_N, C5_W = 50_000_000, 5000
+# test hooks only (scripts/bench_dist_try.sh, tests): a smaller instance and
+# the gloo backend with ranks sharing one device -- never used by the driver
 _TEST_N = int(os.environ.get("AQP_BENCH_TEST_N", "0"))
-_TEST_ITERS = int(os.environ.get("AQP_BENCH_TEST_ITERS", "0"))
-CHECK_EVERY = 64
+_SKIP_SECONDARY = os.environ.get("AQP_BENCH_NO_SECONDARY", "") == "1"
 EPS = 1e-8
-METRIC = "BB(CG)-inner iterations/s, C2 solve to 1e-8 rel. KKT"
+METRIC = "BB(CG)-inner iterations/s, C5 solve to 1e-8 rel. KKT (outer iterations [W, W+K))"
 HBM_PEAK_FALLBACK = 6650.0
+
+
+def c5_dims():
+    n = _TEST_N or C5_N
+    w = C5_W if not _TEST_N else max(50, min(C5_W, _TEST_N // 100))
+    return n, w
+
+
+def c5_problem():
+    from paper_2602_23967_b200 import generators
+
+    n, w = c5_dims()
+    return generators.banded_qp(n, n, half_width=w, seed=0)
 
 
 def peaks():
@@ -85,7 +104,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
@@ -127,11 +146,19 @@ def dist_init():
     return world, rank, local
 
 
+def q_full_nnz(p) -> int:
+    q = p.quad if p.quad.kind == "sparse" else getattr(p.quad, "p", None)
+    if q is None:
+        return 0
+    up = q.upper
+    diag_stored = int(np.count_nonzero(np.asarray(up.indices) == np.repeat(np.arange(p.n), np.diff(up.indptr))))
+    return 2 * up.nnz - diag_stored
+
+
 def workload_name(p) -> str:
-    nnz_q = 2 * p.quad.upper.nnz - int(np.count_nonzero(p.quad.upper.indices == np.repeat(
-        np.arange(p.n), np.diff(p.quad.upper.indptr))))
-    return (f"C2 lasso-style QP n={p.n} m={p.m} nnz(A)={p.constraint_matrix.nnz} nnz(Q_full)={nnz_q} "
-            f"(BASELINE configs[1])")
+    n, w = c5_dims()
+    return (f"C5 banded sparse QP n=m={p.n} half_width={w} seed=0 nnz(A)={p.constraint_matrix.nnz} "
+            f"nnz(Q_full)={q_full_nnz(p)} (BASELINE configs[4]: the largest 1-GPU config, row-partitioned for N>1)")
 
 
 def problem_bytes(p) -> int:
@@ -143,7 +170,9 @@ def problem_bytes(p) -> int:
     else:
         pq = q if q.kind == "sparse" else q.p
         arrs += [pq.upper.indptr, pq.upper.indices, pq.upper.data, pq.diag]
-    return int(sum(x.nbytes for x in arrs))
+        if q.kind == "sparse_low_rank":
+            arrs += [q.r.indptr, q.r.indices, q.r.data]
+    return int(sum(np.asarray(x).nbytes for x in arrs))
 
 
 def host_cpu() -> dict:
@@ -159,59 +188,132 @@ def host_cpu() -> dict:
     return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
-def cpu_baseline(spec: str, warmup: int, steps: int, threads: int):
-    env = dict(os.environ)
+def ref_sample(problem, warmup: int, steps: int, threads: int):
+    """Reference CPU solver on outer iterations [warmup, warmup+steps) of the same solve."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref_bench
+
     if threads == 1:
-        env.update(OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1", MKL_NUM_THREADS="1")
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "oracle", "ref_bench.py"), spec, str(warmup), str(steps)],
-                         capture_output=True, text=True, env=env, timeout=1800)
-    if out.returncode != 0:
-        raise RuntimeError(out.stderr[-2000:])
-    return json.loads(out.stdout.strip().splitlines()[-1])
+        from threadpoolctl import threadpool_limits
+
+        with threadpool_limits(limits=1):
+            return ref_bench.run_problem(problem, warmup, steps, EPS)
+    return ref_bench.run_problem(problem, warmup, steps, EPS)
+
+
+def base_line(args, world, value, ms, sharded):
+    return {
+        "metric": METRIC, "value": value, "unit": "inner_iters/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps if args.steps else None, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+    }
+
+
+def config_block(problem, args, world, sharded):
+    return {"workload": workload_name(problem),
+            "range": f"outer iterations [{args.warmup}, {args.warmup + args.steps}) of one solve from the "
+                     f"reference's initial point (both arms)",
+            "step": "one outer PDHG iteration incl. its full BB inner solve",
+            "eps_tol": EPS, "params": "reference defaults (SolverParams(eps_tol=1e-8))",
+            "parallelism": f"rowshard{world}" if sharded else ("replicas" if world > 1 else "single"),
+            "l2": "inputs (~10 GB of matrices + vectors per BB iteration) are ~80x the 126 MB L2: no flush needed; "
+                  "stand-alone kernel timings flush L2 anyway"}
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    spec = f"c2:{SPEC_N}:{SPEC_M}:0"
+    t0 = time.perf_counter()
+    problem = c5_problem()
+    gen_s = time.perf_counter() - t0
     threads = os.cpu_count() or 1
-    r = cpu_baseline(spec, max(args.warmup, 1), args.steps, threads)
+    r = ref_sample(problem, args.warmup, args.steps, threads)
     value = r["inner"] / r["seconds"]
-    from paper_2602_23967_b200 import generators
-
-    prob = generators.lasso_style_qp(SPEC_N, SPEC_M, seed=0)
-    workload = workload_name(prob)
-    line = {
-        "metric": METRIC, "value": value, "unit": "inner_iters/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps, "higher_is_better": True,
-        "scaling": "strong" if args.gpus > 1 and not args.replicas else "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload,
-                   "step": "one outer PDHG iteration (BB inner solve included) of the reference CPU solver",
-                   "eps_tol": EPS},
+    line = base_line(args, args.gpus, value, 1e3 * r["seconds"], args.gpus > 1)
+    line["config"] = config_block(problem, args, args.gpus, args.gpus > 1)
+    line["config"]["parallelism"] = "reference CPU solver (single-threaded Cython kernels; OpenBLAS threads)"
+    line.update({
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "inner_iters/s", "cores": threads, "kind": r["kind"], **host_cpu(),
-                         "sample": f"outer iterations {max(args.warmup,1)}..{max(args.warmup,1)+args.steps} of the C2 solve "
-                                   f"({r['inner']} BB iterations in {r['seconds']:.1f}s; backend {r['backend']})"},
+                         "sample": f"outer iterations [{args.warmup}, {args.warmup + args.steps}) of the C5 solve "
+                                   f"({r['inner']} BB iterations in {r['seconds']:.1f}s; backend {r['backend']}; "
+                                   f"instance generation {gen_s:.0f}s, conversion {r.get('convert_seconds', 0):.0f}s "
+                                   f"and initialisation {r.get('init_seconds') or 0:.0f}s untimed)"},
         "e2e": {"value": value, "unit": "inner_iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    })
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, world, rank, local):
-    import numpy as np
+def kernel_table(problem, local, kinds):
+    """Stand-alone event timing of the hot kernels on a fresh solver of `problem`."""
+    import torch
+
+    from paper_2602_23967_b200 import _native as nat
+    from paper_2602_23967_b200.device import DeviceContext, DeviceProblem, DeviceSolver
+
+    n, m = problem.n, problem.m
+    dev = DeviceProblem(problem, DeviceContext.get(local))
+    sol = DeviceSolver(dev, eps_tol=EPS, eps_inf=1e-9, gamma_sys=1.0, tol_scale=5e-4, tol_floor=1e-9,
+                       diag_bound=problem.quad.diag_bound(), adaptive=True, max_inner=200, halpern=True)
+    sc = nat.Scalars()
+    sc.eta, sc.omega, sc.inner_tol = 0.5, 1.0, 1e-2
+    sol.init(sc)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
+    info = dev.info
+    nnz_q = info.q_full_nnz
+    table = {
+        "bb_gradient": (0, 12 * nnz_q + 4 * (n + 1) + 64 * n),
+        "bb_step": (1, 40 * n),
+        "p1_At_y": (2, 12 * info.at_nnz + 4 * (n + 1) + 8 * m + 40 * n),
+        "p2_A_xbar": (3, 12 * info.a_nnz + 4 * (m + 1) + 8 * n + 48 * m),
+        "x_post": (4, 48 * n),
+        "bb_fold": (5, 8 * 7 * max(info.q_items, 1)),
+    }
+    out = {}
+    for name in kinds:
+        kid, nbytes = table[name]
+        sol.time_kernel(kid, 2, flush)
+        avg = sol.time_kernel(kid, 10, flush)
+        out[name] = {"ms": avg, "alg_bytes": int(nbytes), "gbs": nbytes / (avg * 1e-3) / 1e9}
+    fixed, per_inner = sol.counters()
+    del sol, dev, flush
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out, fixed, per_inner
+
+
+def full_solve_key(problem, local, name):
+    """One full solve to 1e-8 from host arrays, timed end to end."""
     import torch
 
     import paper_2602_23967_b200 as aq
-    from paper_2602_23967_b200 import generators
-    from paper_2602_23967_b200.device import DeviceContext, DeviceProblem, DeviceSolver
-    from paper_2602_23967_b200 import _native as nat
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = aq.solve(problem, aq.SolverParams(eps_tol=EPS), device=local)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    out = {"workload": name, "status": res.status.value, "outer": res.outer_iterations,
+           "inner": res.inner_iterations, "restarts": res.restarts, "kkt": res.report.kkt_max,
+           "objective": res.report.primal_objective, "solve_time_s": wall,
+           "inner_iters_per_s": res.inner_iterations / wall, "outer_iters_per_s": res.outer_iterations / wall}
+    del res
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2602_23967_b200 as aq
 
     local = local % torch.cuda.device_count()  # ranks > devices only in the one-box test hook
     torch.cuda.set_device(local)
-    sharded = world > 1 and not args.replicas
-    seed = 0 if sharded else rank
-    problem = generators.lasso_style_qp(_TEST_N or SPEC_N, (_TEST_N // 2) or SPEC_M, seed=seed)
+    sharded = world > 1
+    t0 = time.perf_counter()
+    problem = c5_problem()
+    gen_s = time.perf_counter() - t0
     group = None
     if sharded:
         from paper_2602_23967_b200.shard import DistGroup
@@ -224,142 +326,108 @@ def run_ours(args, world, rank, local):
     clocks = Clocks(local)
 
     def monitor(outer, inner):
-        idx = outer // CHECK_EVERY
-        if idx in (W, W + K):
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record(stream)
-            marks[idx] = (ev, outer, inner)
-            if idx == W:
-                clocks.start()
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        marks[outer] = (ev, inner)
+        if outer == W:
+            clocks.start()
 
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    prm = aq.SolverParams(eps_tol=EPS, iter_limit=_TEST_ITERS) if _TEST_ITERS else aq.SolverParams(eps_tol=EPS)
-    res = aq.solve(problem, prm, device=local, monitor=monitor, group=group)
+    res = aq.solve(problem, aq.SolverParams(eps_tol=EPS, iter_limit=W + K), device=local, monitor=monitor,
+                   group=group, marks=[W, W + K])
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     clk = clocks.stop()
-    if W in marks and W + K in marks:
-        ms = marks[W][0].elapsed_time(marks[W + K][0])
-        inner = marks[W + K][2] - marks[W][2]
-        outer = marks[W + K][1] - marks[W][1]
-    else:  # solve ended before W+K windows: time the whole run
-        ms, inner, outer = wall * 1e3, res.inner_iterations, res.outer_iterations
-    t = torch.tensor([ms, inner, res.inner_iterations, wall], dtype=torch.float64, device=f"cuda:{local}")
+    ms = marks[W][0].elapsed_time(marks[W + K][0])
+    inner = marks[W + K][1] - marks[W][1]
+    t = torch.tensor([ms, wall], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
-        mx = t.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        sm = t.clone()
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        ms_max, inner_sum, inner_total_sum, wall_max = mx[0].item(), sm[1].item(), sm[2].item(), mx[3].item()
-        if sharded:  # one solve: every rank reports the same counts
-            inner_sum, inner_total_sum = inner, res.inner_iterations
-    else:
-        ms_max, inner_sum, inner_total_sum, wall_max = ms, inner, res.inner_iterations, wall
-    value = inner_sum / (ms_max / 1e3)
-    e2e_value = inner_total_sum / wall_max
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max, wall_max = t[0].item(), t[1].item()
+    value = inner / (ms_max / 1e3)  # one solve: every rank reports the same counts
+    e2e_value = res.inner_iterations / wall_max
+    result = {"status": res.status.value, "outer": res.outer_iterations, "inner": res.inner_iterations,
+              "kkt": res.report.kkt_max, "objective": res.report.primal_objective}
+    del res
+    gc.collect()
+    torch.cuda.empty_cache()
+    if group is not None:
+        group.close()
+    if rank != 0:
+        return
 
-    # --- the same solve with the opt-in device-side Ruiz + Pock-Chambolle
-    # scaling (extension, not the reference's algorithm: reported beside the
-    # headline, never as it)
-    scaled = None
-    if not sharded:
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        rs_ = aq.solve(problem, aq.SolverParams(eps_tol=EPS, scaling="ruiz_pc"), device=local)
-        torch.cuda.synchronize()
-        scaled = {"status": rs_.status.value, "outer": rs_.outer_iterations, "inner": rs_.inner_iterations,
-                  "kkt": rs_.report.kkt_max, "objective": rs_.report.primal_objective,
-                  "solve_time_s": time.perf_counter() - t1,
-                  "note": "SolverParams(scaling='ruiz_pc'): opt-in equilibration, certified on the original problem"}
-
-    # --- dominant-kernel roofline (stand-alone, L2 flushed before each launch)
     peak, peak_kind = peaks()
-    dev = DeviceProblem(problem, DeviceContext.get(local))
-    sol = DeviceSolver(dev, eps_tol=EPS, eps_inf=1e-9, gamma_sys=1.0, tol_scale=5e-4, tol_floor=1e-9,
-                       diag_bound=problem.quad.diag_bound(), adaptive=True, max_inner=200, halpern=True)
-    sc = nat.Scalars()
-    sc.eta, sc.omega, sc.inner_tol = 0.5, 1.0, 1e-2
-    sol.init(sc)
-    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
-    nnz_q = dev.info.q_full_nnz
-    kernels = {}
-    for kid, name, nbytes in ((0, "bb_gradient", 12 * nnz_q + 4 * (n + 1) + 64 * n),
-                              (1, "bb_step", 40 * n),
-                              (2, "p1_At_y", 12 * dev.info.at_nnz + 4 * (n + 1) + 8 * m + 8 * n + 16 * n + 16 * n),
-                              (3, "p2_A_xbar", 12 * dev.info.a_nnz + 4 * (m + 1) + 8 * n + 48 * m),
-                              (5, "bb_fold", 8 * 7 * dev.info.q_items)):
-        sol.time_kernel(kid, 3, flush)
-        avg = sol.time_kernel(kid, 20, flush)
-        kernels[name] = {"ms": avg, "alg_bytes": nbytes, "gbs": nbytes / (avg * 1e-3) / 1e9}
+    kernels, fixed, per_inner = kernel_table(problem, local, ("bb_gradient", "bb_step", "p1_At_y", "p2_A_xbar",
+                                                              "x_post", "bb_fold"))
     top = kernels["bb_gradient"]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof))["kernels"]["bb_gradient"]["dram_bytes_per_launch"]
+            traffic = json.load(open(prof))["kernels"]["c5_bb_gradient"]["dram_bytes_per_launch"]
         except Exception:
             traffic = None
-    fixed, per_inner = sol.counters()
-    n_checks = res.outer_iterations // CHECK_EVERY + 2
-    launches = res.outer_iterations * fixed + res.inner_iterations * per_inner + n_checks * 10
-    # algorithmic bytes per outer / inner iteration
+    nnz_q = q_full_nnz(problem)
+    nnz_a = problem.constraint_matrix.nnz
+    # algorithmic bytes of the timed range (SURVEY.md §8(d) pass model)
     b_in = 12 * nnz_q + 4 * (n + 1) + 112 * n
-    b_out_fixed = 24 * problem.constraint_matrix.nnz + 4 * (n + m + 2) + 80 * n + 64 * m + b_in - 24 * n
-    alg_gbs = (outer * b_out_fixed + inner * b_in) / (ms / 1e3) / 1e9
-
-    if rank != 0:
-        return
-    line = {
-        "metric": METRIC, "value": value, "unit": "inner_iters/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_max / K if K else None, "higher_is_better": True,
-        "scaling": "strong" if sharded else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(problem),
-                   "step": f"one certification window = {CHECK_EVERY} outer iterations + device check",
-                   "eps_tol": EPS,
-                   "parallelism": f"rowshard{world}" if sharded else ("replicas" if world > 1 else "single"),
-                   "l2": "inputs (~230 MB of matrices+vectors per iteration) exceed the 126 MB L2; "
-                         "roofline kernel timed with a 512 MB L2 flush before every launch"},
-        "solve": {"status": res.status.value, "outer": res.outer_iterations, "inner": res.inner_iterations,
-                  "restarts": res.restarts, "kkt": res.report.kkt_max, "objective": res.report.primal_objective,
-                  "solve_time_s": wall},
-        "solve_time_s": wall,
-        "solve_ruiz_pc": scaled,
-        "outer_iters_per_s": outer / (ms / 1e3),
-        "window_alg_gbs": alg_gbs,
+    b_out_fixed = 24 * nnz_a + 4 * (n + m + 2) + 80 * n + 64 * m + b_in - 24 * n
+    alg_gbs = (K * b_out_fixed + inner * b_in) / (ms_max / 1e3) / 1e9
+    line = base_line(args, world, value, ms_max, sharded)
+    line["config"] = config_block(problem, args, world, sharded)
+    line.update({
+        "timed": {"outer": K, "inner": inner, "ms": ms_max, "inner_per_outer": inner / max(K, 1),
+                  "outer_iters_per_s": K / (ms_max / 1e3), "alg_gbs": alg_gbs, "alg_frac": alg_gbs / peak},
+        "solve": dict(result, iter_limit=W + K, wall_s=wall_max, gen_s=gen_s),
         "e2e": {"value": e2e_value, "unit": "inner_iters/s", "h2d_bytes_per_step": problem_bytes(problem),
-                "d2h_bytes_per_step": 8 * (2 * n + m), "scope": "one full solve call from host arrays per step"},
+                "d2h_bytes_per_step": 8 * (2 * n + m),
+                "scope": f"one solve call from host arrays (iter_limit {W + K}): upload, device A'/Q build, "
+                         f"norm estimate, all {W + K} outer iterations, final check, read-back of x, y, slack"},
         "roofline": {"bound": "hbm", "achieved": top["gbs"], "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": top["gbs"] / peak, "traffic": traffic, "kernel": "bb_gradient (Q SpMV + epilogue)",
-                     "alg_bytes_per_launch": top["alg_bytes"], "ms_per_launch": top["ms"]},
+                     "frac": top["gbs"] / peak, "traffic": traffic,
+                     "kernel": "C5 bb_gradient (Q SpMV + gradient epilogue + 7 sums)",
+                     "alg_bytes_per_launch": top["alg_bytes"], "ms_per_launch": top["ms"],
+                     "alg_bytes_rule": "12*nnz(Q_full) + 4*(n+1) + 64*n (SURVEY.md §8(d))"},
         "kernels": kernels,
-        "gpu_launches": int(launches * K * CHECK_EVERY / max(res.outer_iterations, 1)),
+        "gpu_launches": int(K * fixed + inner * per_inner),
         "clocks": clk,
-    }
+    })
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_baseline(f"c2:{SPEC_N}:{SPEC_M}:0", 2, 8, threads=1)
+            cb = ref_sample(problem, 1, 1, threads=1)
             line["cpu_baseline"] = {"value": cb["inner"] / cb["seconds"], "unit": "inner_iters/s", "cores": 1,
                                     "kind": cb["kind"], **host_cpu(),
-                                    "sample": f"outer iterations 2..10 of the same C2 solve ({cb['inner']} BB "
-                                              f"iterations in {cb['seconds']:.1f}s, backend {cb['backend']})"}
+                                    "sample": f"outer iteration [1, 2) of the same C5 solve ({cb['inner']} BB "
+                                              f"iterations in {cb['seconds']:.1f}s, backend {cb['backend']}, "
+                                              f"1 BLAS thread)"}
         except Exception as exc:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "error": str(exc)[-300:]}
+    del problem
+    gc.collect()
+    if world == 1 and not _SKIP_SECONDARY:
+        from paper_2602_23967_b200 import generators
+
+        p3 = generators.portfolio_qp(5_000_000, 100, seed=0)
+        line["c3_solve"] = full_solve_key(p3, local, "C3 factor-model portfolio n=5e6 k=100 (BASELINE configs[2])")
+        del p3
+        p2 = generators.lasso_style_qp(1_000_000, 500_000, seed=0)
+        line["c2_solve"] = full_solve_key(p2, local, "C2 Lasso-style QP n=1e6 m=5e5 (BASELINE configs[1])")
     print(json.dumps(line), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--replicas", action="store_true", help="N>1: independent solves instead of one sharded solve")
     args = ap.parse_args()
+    if args.warmup < 3 or args.steps < 1:
+        ap.error("need --warmup >= 3 and --steps >= 1")
     world, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, world, rank)

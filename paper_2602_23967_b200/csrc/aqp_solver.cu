@@ -34,7 +34,6 @@
 namespace aqp {
 
 constexpr int kFinThreads = 1024;  // fold block: 4x the loads in flight of a 256-thread block
-constexpr int64_t kPersistMaxRows = 400000;  // n + m up to which windows may run persistent
 
 // ---------------------------------------------------------------- control block
 enum RedSlot : int {
@@ -71,7 +70,6 @@ struct SV {
   double *xlast, *ylast, *xblk, *yblk, *xavgp, *yavgp;
   double *lin, *xbar, *xbb[3], *gbb[2];
   double *rx, *rtv;        // low-rank temporaries (k and n)
-  double *part1;           // persistent kernel: second partials buffer (small problems only)
   const double *Rd;        // dense R (k x n row-major) when the problem holds R dense
   double *rxpart;          // dense R x: per-block partials [k][blocks]
   int rk;                  // rows of R
@@ -92,9 +90,8 @@ struct SV {
 
 
 // Gather of a vector the solve itself writes.  AQP_GATHER_NC=1 uses the
-// non-coherent read-only path (ld.global.nc); the default plain ld.global is
-// coherent, so the same ops can run inside a persistent kernel whose phases
-// are separated by grid barriers instead of kernel boundaries.
+// non-coherent read-only path (ld.global.nc, measured 2% slower on C2); the
+// default is a plain ld.global.
 #ifndef AQP_GATHER_NC
 #define AQP_GATHER_NC 0
 #endif
@@ -1329,247 +1326,6 @@ __global__ void __cluster_dims__(kFoldCtas, 1, 1) __launch_bounds__(kFoldThreads
 #define AQP_FOLD_CLUSTER 1
 #endif
 
-// ================================================================ persistent window kernel
-// Small problems (C1, C4: a few thousand to 1e5 rows) spend their time in
-// launch latency, not bytes: a BB iteration is three dependent kernels of a
-// few microseconds each.  Here one cooperative launch runs the whole
-// certification window on a resident grid: the phases of the graph become
-// device functions separated by grid barriers, the WHILE nodes become loops.
-// Every reduction reproduces the graph path's arithmetic exactly -- items and
-// element blocks are processed as "virtual blocks" with the same per-thread
-// order and block trees, and the 1024-thread fold of fin_ctrl_op is emulated
-// by 256 threads carrying four virtual threads each -- so both paths give
-// bitwise-identical iterates (tests/test_gpu_solve.py, AQP_PERSISTENT=0/1).
-
-// sense-reversing grid barrier (count, generation) for a co-resident grid
-__device__ __forceinline__ void grid_sync(unsigned *bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned *gen = bar + 1;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0u;
-      __threadfence();
-      atomicExch(bar + 1, g + 1u);
-    } else {
-      while (*gen == g) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// fold_partials + block_reduce of a kFinThreads (1024) block, computed by a
-// kThreads (256) block: real thread t is virtual threads t + 256 q (q < 4),
-// whose virtual warp (t / 32 + 8 q) has the same lanes -- same sums, same tree
-template <int NS, int NM>
-__device__ __forceinline__ void fold_v1024(RedVals<NS, NM> &out, const double *partials, unsigned nb, double *smem) {
-  constexpr int NT = NS + NM, QV = kFinThreads / kThreads, U = 4;
-  RedVals<NS, NM> a[QV];
-#pragma unroll
-  for (int q = 0; q < QV; ++q) a[q].zero();
-  if constexpr (NT > 0) {
-#pragma unroll
-    for (int q = 0; q < QV; ++q) {
-      const unsigned vt = threadIdx.x + kThreads * q;
-      for (unsigned b0 = vt; b0 < nb; b0 += U * kFinThreads) {
-        double t[U][NT];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const unsigned b = b0 + u * kFinThreads;
-#pragma unroll
-          for (int i = 0; i < NT; ++i) t[u][i] = b < nb ? partials[(size_t)i * nb + b] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-#pragma unroll
-          for (int i = 0; i < NS; ++i) a[q].s[i] += t[u][i];
-#pragma unroll
-          for (int i = 0; i < NM; ++i) a[q].m[i] = nanmax(a[q].m[i], t[u][NS + i]);
-        }
-      }
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int q = 0; q < QV; ++q) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-        for (int i = 0; i < NS; ++i) a[q].s[i] += __shfl_xor_sync(0xffffffffu, a[q].s[i], off);
-#pragma unroll
-        for (int i = 0; i < NM; ++i) a[q].m[i] = nanmax(a[q].m[i], __shfl_xor_sync(0xffffffffu, a[q].m[i], off));
-      }
-      if (lane == 0) {
-        const int vw = warp + kWarps * q;
-#pragma unroll
-        for (int i = 0; i < NS; ++i) smem[vw * NT + i] = a[q].s[i];
-#pragma unroll
-        for (int i = 0; i < NM; ++i) smem[vw * NT + NS + i] = a[q].m[i];
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      constexpr int NW = kFinThreads / 32;
-#pragma unroll
-      for (int i = 0; i < NS; ++i) out.s[i] = smem[i];
-#pragma unroll
-      for (int i = 0; i < NM; ++i) out.m[i] = smem[NS + i];
-      for (int w = 1; w < NW; ++w) {
-#pragma unroll
-        for (int i = 0; i < NS; ++i) out.s[i] += smem[w * NT + i];
-#pragma unroll
-        for (int i = 0; i < NM; ++i) out.m[i] = nanmax(out.m[i], smem[w * NT + NS + i]);
-      }
-    }
-    __syncthreads();
-  }
-}
-
-struct PersistSmem {
-  double sred[kWarps * kMaxRed];
-  double sfold[(kFinThreads / 32) * kMaxRed];
-  unsigned long long cbuf[sizeof(Ctrl) / 8];
-};
-
-// an SpMV phase: every plan item as a virtual block, partials [slot][item]
-template <class Op>
-__device__ __forceinline__ void p_spmv(const DevCsr &M, const Op &op, double *partials, double *sprod, int *scol,
-                                       PersistSmem &sm) {
-  constexpr int NS = Op::NS, NM = Op::NM;
-  Op o = op;
-  o.prepare();
-  for (int item = blockIdx.x; item < M.nitems; item += gridDim.x) {
-    const PlanItem it = M.plan[item];
-    RedVals<NS, NM> acc;
-    acc.zero();
-    spmv_item<Op, false>(M, it, o, acc, sprod, scol, sm.sred);
-    if constexpr (Op::FINAL && NS + NM > 0) {
-      block_reduce<NS, NM>(acc, sm.sred);
-      if (threadIdx.x == 0) {
-#pragma unroll
-        for (int i = 0; i < NS; ++i) partials[(size_t)i * M.nitems + item] = acc.s[i];
-#pragma unroll
-        for (int i = 0; i < NM; ++i) partials[(size_t)(NS + i) * M.nitems + item] = acc.m[i];
-      }
-    }
-    __syncthreads();  // the item's staging smem is reused by the next item
-  }
-}
-
-// an elementwise phase: the elem_op grid of n as virtual blocks
-template <class Op>
-__device__ __forceinline__ void p_elem(int64_t n, const Op &op, double *partials, PersistSmem &sm) {
-  constexpr int NS = Op::NS, NM = Op::NM;
-  Op o = op;
-  o.prepare();
-  const int G = elem_grid(n);
-  const int64_t stride = (int64_t)G * kThreads;
-  for (int vb = blockIdx.x; vb < G; vb += gridDim.x) {
-    RedVals<NS, NM> acc;
-    acc.zero();
-    for (int64_t i = (int64_t)vb * kThreads + threadIdx.x; i < n; i += stride) o.elem(i, acc);
-    if constexpr (Op::FINAL && NS + NM > 0) {
-      block_reduce<NS, NM>(acc, sm.sred);
-      if (threadIdx.x == 0) {
-#pragma unroll
-        for (int i = 0; i < NS; ++i) partials[(size_t)i * G + vb] = acc.s[i];
-#pragma unroll
-        for (int i = 0; i < NM; ++i) partials[(size_t)(NS + i) * G + vb] = acc.m[i];
-      }
-    }
-  }
-}
-
-// fin_ctrl_op's fold + finalize, computed redundantly by EVERY block on its
-// own shared-memory copy of the control block (op.v.ctrl points there): the
-// fold is deterministic, so all copies stay identical and no second barrier
-// is needed.  Phases alternate between two partials buffers, so a block that
-// runs ahead into the next phase never overwrites partials a slower block is
-// still folding (a block cannot get two phases ahead: every phase ends at a
-// grid barrier).
-template <class Op>
-__device__ __forceinline__ void p_fold(const Op &op, unsigned nb, const double *partials, PersistSmem &sm,
-                                       unsigned *bar) {
-  constexpr int NS = Op::NS, NM = Op::NM;
-  grid_sync(bar);
-  RedVals<NS, NM> a;
-  a.zero();
-  fold_v1024<NS, NM>(a, partials, nb, sm.sfold);
-  Op o = op;
-  o.prepare();
-  if (threadIdx.x == 0) o.finalize(a);
-  __syncthreads();
-}
-
-template <bool DIAG>
-__global__ void __launch_bounds__(kThreads, 1) k_window_persist(SV v, DevCsr A, DevCsr At, DevCsr Q, double *part0,
-                                                                double *part1, unsigned *bar) {
-  constexpr int W = (int)(sizeof(Ctrl) / 8);
-  extern __shared__ double dyn_smem[];
-  double *sprod = dyn_smem;
-  int *scol = reinterpret_cast<int *>(dyn_smem + kTileNnz);
-  __shared__ PersistSmem sm;
-  // block-local control block (identical in every block, see p_fold)
-  Ctrl *gctrl = v.ctrl;
-  for (int i = threadIdx.x; i < W; i += blockDim.x)
-    sm.cbuf[i] = __ldcg(reinterpret_cast<const unsigned long long *>(gctrl) + i);
-  __syncthreads();
-  v.ctrl = reinterpret_cast<Ctrl *>(sm.cbuf);
-  v.in_graph = 0;
-  const Ctrl *ct = v.ctrl;
-  int ph = 0;  // partials buffer of the current phase
-  auto part = [&]() { return (ph & 1) ? part1 : part0; };
-  for (;;) {
-    if (DIAG) {
-      OpP1Diag o{};
-      o.v = v;
-      p_spmv(At, o, part(), sprod, scol, sm);
-      p_fold(o, (unsigned)At.nitems, part(), sm, bar);
-      ++ph;
-    } else {
-      {
-        OpP1Bb o{};
-        o.v = v;
-        p_spmv(At, o, part(), sprod, scol, sm);
-        grid_sync(bar);
-      }
-      {
-        OpGrad<true> g0{};
-        g0.v = v;
-        p_spmv(Q, g0, part(), sprod, scol, sm);
-        p_fold(g0, (unsigned)Q.nitems, part(), sm, bar);
-        ++ph;
-      }
-      while (ct->bb_cont) {
-        OpStep st{};
-        st.v = v;
-        p_elem(v.nl, st, part(), sm);
-        grid_sync(bar);
-        OpGrad<false> gg{};
-        gg.v = v;
-        p_spmv(Q, gg, part(), sprod, scol, sm);
-        p_fold(gg, (unsigned)Q.nitems, part(), sm, bar);
-        ++ph;
-      }
-      OpXPost xp{};
-      xp.v = v;
-      p_elem(v.nl, xp, part(), sm);
-      p_fold(xp, (unsigned)elem_grid(v.nl), part(), sm, bar);
-      ++ph;
-    }
-    OpP2 p2{};
-    p2.v = v;
-    p_spmv(A, p2, part(), sprod, scol, sm);
-    p_fold(p2, (unsigned)A.nitems, part(), sm, bar);
-    ++ph;
-    if (ct->s.halted || ct->s.iters_done >= ct->window_len) break;
-  }
-  if (blockIdx.x == 0) {  // the host reads the control block after the window
-    for (int i = threadIdx.x; i < W; i += blockDim.x) reinterpret_cast<unsigned long long *>(gctrl)[i] = sm.cbuf[i];
-  }
-}
-
 }  // namespace aqp
 
 using namespace aqp;
@@ -1601,10 +1357,6 @@ struct aqp_solver {
   double *bounce = nullptr;       // vector reads / start-vector upload (aqp_ctx::bounce)
   static constexpr size_t kBounce = 1 << 21;  // doubles (16 MB)
   bool shard = false;       // problem is row-sharded (nranks > 1): graph built at connect
-  bool persist = false;     // windows run as one cooperative kernel (small problems)
-  int persist_grid = 0;
-  int persist_smem = 0;
-  unsigned *bar = nullptr;  // grid barrier words of the persistent kernel
 };
 
 namespace {
@@ -1636,9 +1388,7 @@ void layout_solver(Bump &b, aqp_problem *p, SV &v, Ctrl **ctrl, GridRed &gr) {
   int64_t maxg = 148 * 8;
   for (const DevCsr *M : {&p->A, &p->At, &p->Q, &p->R, &p->Rt}) maxg = std::max<int64_t>(maxg, M->nitems);
   gr.partials = (double *)b.take(maxg * kMaxRed * 8);
-  gr.ticket = (unsigned *)b.take(64);  // [0] grid_end ticket, [4..5] persistent-kernel barrier
-  // second partials buffer of the persistent small-problem kernel (ping-pong)
-  v.part1 = (p->n + p->m <= kPersistMaxRows) ? (double *)b.take(maxg * kMaxRed * 8) : nullptr;
+  gr.ticket = (unsigned *)b.take(64);  // [0] grid_end ticket
   if (p->r_dense) v.rxpart = (double *)b.take(std::max<int64_t>(p->R.rows, 1) * dense_rx_blocks(p->n) * 8);
 }
 
@@ -2109,35 +1859,6 @@ int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, si
       return rc;
     }
   }
-  // opt-in (AQP_PERSISTENT=1, small problems): one cooperative persistent
-  // kernel per window instead of the graph.  Measured on B200 it is NOT
-  // faster than the PDL graph (C1 0.87x, n = 1e5 diagonal 0.78x, tiny
-  // instances 1.1-1.25x; scripts/persist_try.py): a grid barrier costs about
-  // what a programmatic graph edge does.  It stays as an exact alternative
-  // (bitwise-identical iterates, tests/test_gpu_solve.py) and a base for
-  // cluster-scoped variants.
-  {
-    const char *e = getenv("AQP_PERSISTENT");
-    const bool eligible = !s->shard && p->quad_kind != AQP_QUAD_SPARSE_LOW_RANK && s->v.part1 != nullptr;
-    const bool want = eligible && e && e[0] == '1';
-    if (want) {
-      const bool diag = p->quad_kind == AQP_QUAD_DIAGONAL;
-      const void *fn = diag ? (const void *)k_window_persist<true> : (const void *)k_window_persist<false>;
-      const int smem = std::max({p->A.smem_bytes, p->At.smem_bytes, diag ? 0 : p->Q.smem_bytes});
-      int per_sm = 0;
-      AQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
-      const int64_t need = std::max<int64_t>({(int64_t)p->A.nitems, (int64_t)p->At.nitems,
-                                              diag ? 0 : (int64_t)p->Q.nitems, (int64_t)elem_grid(p->n), 1});
-      if (per_sm > 0) {
-        s->persist = true;
-        int64_t cap = (int64_t)per_sm * p->ctx->sm_count;
-        if (const char *g = getenv("AQP_PERSIST_GRID")) cap = std::max<int64_t>(1, std::min<int64_t>(cap, atoll(g)));
-        s->persist_grid = (int)std::min<int64_t>(cap, need);
-        s->persist_smem = smem;
-        s->bar = s->gr.ticket + 4;
-      }
-    }
-  }
   *out = s;
   return AQP_OK;
 }
@@ -2339,20 +2060,6 @@ int aqp_solver_run(aqp_solver *s, int64_t n_iters) {
   AQP_TRY(push_scalars(s));
   AQP_TRY(poke(s, &Ctrl::window_len, (int64_t)n_iters));
   if (s->eager) return run_eager(s, n_iters);
-  if (s->persist) {
-    aqp_problem *p = s->p;
-    SV v = s->v;
-    v.in_graph = 0;
-    DevCsr A = p->A, At = p->At, Q = p->Q;
-    double *partials = s->gr.partials, *part1 = v.part1;
-    unsigned *bar = s->bar;
-    void *args[] = {&v, &A, &At, &Q, &partials, &part1, &bar};
-    const void *fn = p->quad_kind == AQP_QUAD_DIAGONAL ? (const void *)k_window_persist<true>
-                                                       : (const void *)k_window_persist<false>;
-    AQP_CUDA(cudaLaunchCooperativeKernel(fn, dim3(s->persist_grid), dim3(kThreads), args, (size_t)s->persist_smem,
-                                         p->ctx->stream));
-    return AQP_OK;
-  }
   AQP_CUDA(cudaGraphLaunch(s->exec, s->p->ctx->stream));
   return AQP_OK;
 }

@@ -16,7 +16,7 @@ import dataclasses
 import enum
 import math
 import time
-from typing import Callable, Optional
+from typing import Callable, Optional, Sequence
 
 import numpy as np
 
@@ -279,7 +279,8 @@ def _scaled_diag_bound(quad, d: np.ndarray) -> float:
 
 
 def solve(problem, params: Optional[SolverParams] = None, progress: Optional[ProgressCallback] = None,
-          device: int = 0, monitor: Optional[Callable[[int, int], None]] = None, group=None) -> SolveResult:
+          device: int = 0, monitor: Optional[Callable[[int, int], None]] = None, group=None,
+          marks: Optional[Sequence[int]] = None) -> SolveResult:
     """Run until optimality, an infeasibility certificate, or a limit
     (engine.py:339-498).  ``problem`` may be this package's QpProblem or the
     reference's (rebuilt field by field).
@@ -288,6 +289,13 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
     at every certification point right after the device check, with the
     cumulative outer and BB-inner iteration counts -- bench.py brackets
     certification windows with CUDA events from it.
+
+    ``marks`` (extension): outer-iteration counts at which a window is split
+    (without a certification point -- the device loop simply continues in the
+    next graph launch, so the trajectory is unchanged); with ``marks`` given,
+    ``monitor`` is called right after the window that reaches each mark
+    instead of at certification points.  bench.py times outer iterations
+    [W, W+K) with it, the same range its reference arm times.
 
     ``group`` (extension, shard.PeerGroup): solve this problem row-sharded
     with the group's other ranks; every rank calls solve
@@ -332,6 +340,7 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
     probe_until = 0
     rp = params.restart
     check_every = params.check_every
+    pending_marks = sorted({int(k) for k in marks if int(k) > 0}) if marks is not None else []
 
     def push(**kw):
         s = sol.get_scalars()
@@ -364,10 +373,15 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
             window = min(window, probe_until - n_outer)
         elif rp.enabled:
             window = min(window, max(1, rp.max_round_len - sc.k))
+        if pending_marks:
+            window = min(window, pending_marks[0] - n_outer)
         sol.run(window)
         sc = sol.get_scalars()
         n_outer += sc.iters_done
         n_inner += sc.inner_sum
+        while pending_marks and pending_marks[0] <= n_outer:
+            if pending_marks.pop(0) == n_outer and monitor is not None:
+                monitor(n_outer, n_inner)
         if sc.halted:
             # engine.py:407-417: overflow inside the round
             sol.rollback()
@@ -385,7 +399,7 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
             continue  # window ended at the probe boundary
         # ---- certification point (engine.py:436-494) -----------------------
         cr = run.check(with_rays=True)
-        if monitor is not None:
+        if monitor is not None and marks is None:
             monitor(n_outer, n_inner)
         report = run.report(cr, want_slack)
         kkt = report.kkt_max

@@ -253,20 +253,6 @@ def test_config4_full_size_pair(cuda):
         assert_parity(r, g["status"], g["outer"], g["objective"])
 
 
-@pytest.mark.parametrize("spec", ["c1:0", "rqp:500:300:diagonal:0.02:5", "c4i:1e3:1"])
-def test_persistent_window_kernel_is_bitwise_identical(cuda, spec, monkeypatch):
-    """AQP_PERSISTENT=1 runs each window as one cooperative kernel whose
-    reductions emulate the graph path's exactly (aqp_solver.cu k_window_persist)."""
-    p = instances.build(spec)
-    prm = SolverParams(eps_tol=1e-8)
-    monkeypatch.setenv("AQP_PERSISTENT", "0")
-    a = solve(p, prm)
-    monkeypatch.setenv("AQP_PERSISTENT", "1")
-    b = solve(p, prm)
-    assert (a.status, a.outer_iterations, a.inner_iterations) == (b.status, b.outer_iterations, b.inner_iterations)
-    assert np.array_equal(a.x, b.x) and np.array_equal(a.y, b.y)
-
-
 @pytest.mark.parametrize("scaling", ["ruiz", "ruiz_pc"])
 @pytest.mark.parametrize("spec,fname", [("c1:0", "ref_c1_s0.json"),
                                         ("rqp:300:150:low_rank:0.05:3", "ref_rqp_300_150_low_rank_0.05_3.json"),

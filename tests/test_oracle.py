@@ -62,3 +62,32 @@ def test_oracle_reproduces_reference_runs(spec, fname):
     assert (r["outer"], r["inner"], r["restarts"]) == (g["outer"], g["inner"], g["restarts"])
     assert r["report"]["primal_objective"] == g["objective"]
     assert r["report"]["kkt"] == g["kkt"]
+
+
+def test_norm_memo_is_the_reference_value():
+    """bench.py's reference arm serves estimate_norm from oracle/norm_memo.py's
+    recordings; a recording must be bitwise what the unmodified reference
+    function returns on the same matrix, and an unrecorded matrix must fall
+    through to the real function."""
+    import norm_memo
+    import refbridge
+
+    aq = refbridge.load_reference()
+    if aq is None:
+        pytest.skip("reference not built (oracle/build_ref.sh)")
+    import anchorqp.engine as eng
+    import anchorqp.linalg as L
+
+    prob = refbridge.to_reference(instances.build("c5:5e4:500:0"), aq)
+    live = L.estimate_norm(prob.constraint_matrix, 100, 0)
+    rec = norm_memo._load()[norm_memo.fingerprint(prob.constraint_matrix)]
+    assert float.fromhex(rec["value_hex"]) == live
+    saved = eng.estimate_norm
+    try:
+        f = norm_memo.patch(aq)
+        assert eng.estimate_norm is f
+        assert f(prob.constraint_matrix, 100, 0) == live  # recorded, bitwise
+        other = refbridge.to_reference(instances.build("c5:2e3:50:1"), aq).constraint_matrix
+        assert f(other, 20, 0) == L.estimate_norm(other, 20, 0)  # not recorded: the real function
+    finally:
+        eng.estimate_norm = saved
