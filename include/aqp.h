@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define AQP_ABI_VERSION 1
+#define AQP_ABI_VERSION 2
 
 enum {
   AQP_OK = 0,
@@ -97,9 +97,40 @@ int aqp_ctx_destroy(aqp_ctx *ctx);
 /* ------------------------------------------------------------------------ */
 /* problem: device copy of QpProblem (reference model.py:124-165)            */
 /* ------------------------------------------------------------------------ */
+/* Storage shard of a row-partitioned problem (the
+ * reference has no multi-GPU path -- its only parallelism is a process pool
+ * over instances, anchorqp/bench.py:89-98).  Rank `rank` of `nranks` (<= 8)
+ * owns rows [n0,n1) of A' and of the full symmetric Q (x side) and rows
+ * [m0,m1) of A (y side), and stores ONLY those: with a shard descriptor the
+ * aqp_problem_desc arrays are this rank's blocks (see aqp_problem_desc).
+ * Gathered vectors live in per-rank windows [xw[2r], xw[2r+1]) /
+ * [yw[2r], yw[2r+1]) that cover the rank's own rows and every column its
+ * rows gather; column indices stay global.  All ranks pass identical xw /
+ * yw tables (they size the peer-visible exchange region identically). */
+typedef struct {
+  int32_t rank, nranks;
+  int64_t n0, n1, m0, m1;   /* owned rows */
+  int64_t a_row0, a_rows;   /* the uploaded A block: rows [a_row0, a_row0 + a_rows) of A, covering
+                               [m0,m1) and every row with a nonzero in columns [n0,n1) */
+  int64_t q_row0;           /* the uploaded P block: upper-triangle rows [q_row0, n1), covering every
+                               row with an upper entry in columns [n0,n1) */
+  int64_t a_local_nnz;      /* nonzeros of A rows [m0,m1) */
+  int64_t at_local_nnz;     /* nonzeros of the A block in columns [n0,n1) (= nnz of A' rows [n0,n1)) */
+  int64_t q_local_nnz;      /* nonzeros of full symmetric Q rows [n0,n1) (diagonal included) */
+  int64_t xw[16], yw[16];   /* gather windows of every rank: [lo, hi) pairs, rank-major */
+  int64_t nl_cap, ml_cap;   /* max over ranks of n1-n0 and m1-m0 */
+} aqp_shard_desc;
+
 /* All array pointers are DEVICE pointers to the reference layouts
  * (CSR int64 indptr/indices, float64 values, float64 vectors), already in
- * HBM.  They are read during aqp_problem_create only. */
+ * HBM.  They are read during aqp_problem_create only.
+ *
+ * With `shard` set (a row shard, see aqp_shard_desc) the arrays are this
+ * rank's blocks, indices global: a_* = the A block (a_rows rows), q_* = the
+ * upper-triangle P block (rows [q_row0, n1)), q_values / q_diag / cost /
+ * var_lo / var_hi = entries [n0,n1), con_lo / con_hi = entries [m0,m1),
+ * r_* = columns [n0,n1) of R (dense: r_rows x (n1-n0) row-major; CSR:
+ * r_rows rows with global column indices). */
 typedef struct {
   int64_t n, m;
   /* A: m x n CSR (linalg.py:28-112) */
@@ -134,6 +165,7 @@ typedef struct {
   const double *var_hi; /* n */
   const double *con_lo; /* m */
   const double *con_hi; /* m */
+  const aqp_shard_desc *shard; /* NULL: the whole problem on this device */
 } aqp_problem_desc;
 
 typedef struct {
@@ -148,26 +180,14 @@ typedef struct aqp_problem aqp_problem;
  * the transient scratch (needed only inside aqp_problem_create). */
 int aqp_problem_sizes(const aqp_problem_desc *desc, size_t *persistent_bytes, size_t *scratch_bytes);
 /* host_a_indptr / host_q_indptr / host_r_indptr: HOST copies of the indptr
- * arrays (used to plan the SpMV work partition; may be NULL for absent parts). */
+ * arrays (used to plan the SpMV work partition; may be NULL for absent parts;
+ * for a shard: of the uploaded blocks). */
 int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *desc,
                        const int64_t *host_a_indptr, const int64_t *host_q_indptr,
                        const int64_t *host_r_indptr,
                        void *persistent, size_t persistent_bytes,
                        void *scratch, size_t scratch_bytes, aqp_problem **out);
 int aqp_problem_get_info(const aqp_problem *p, aqp_problem_info *out);
-
-/* Row shard of a multi-GPU solve (the reference has no
- * multi-GPU path -- its only parallelism is a process pool over instances,
- * anchorqp/bench.py:89-98).  Rank `rank` of `nranks` (<= 8) owns rows
- * [n0,n1) of A' and Q (x side) and rows [m0,m1) of A (y side); every rank
- * creates the whole problem, then restricts its passes to its rows.  Not
- * available for the low-rank Q kind. */
-typedef struct {
-  int32_t rank, nranks;
-  int64_t n0, n1;
-  int64_t m0, m1;
-} aqp_shard;
-int aqp_problem_shard(aqp_problem *p, const aqp_shard *sh);
 
 /* Device-side Ruiz (ruiz_iters rounds of inf-norm equilibration of
  * K = [[Q, A'], [A, 0]]) and optional Pock-Chambolle (alpha = 1, l1) scaling,
@@ -245,7 +265,8 @@ int aqp_solver_destroy(aqp_solver *s);
 int aqp_solver_import_scaled(aqp_solver *dst, aqp_solver *src, const double *D, const double *E);
 /* Row shards: the front of the solver workspace (every gathered vector and
  * the exchange mailbox) is written by the peers; its layout is identical on
- * every rank.  After every rank's aqp_solver_create has returned (host
+ * every rank (buffers are sized by the shard descriptor's max-over-ranks
+ * capacities).  After every rank's aqp_solver_create has returned (host
  * barrier), pass each rank's mapping of its peers' workspace bases
  * (peer_bases[rank] = this workspace; CUDA IPC mappings across processes,
  * plain pointers for ranks sharing a device).  Builds the window graph.
@@ -253,11 +274,11 @@ int aqp_solver_import_scaled(aqp_solver *dst, aqp_solver *src, const double *D, 
  * same calls in the same order. */
 int aqp_solver_exchange_region(aqp_solver *s, void **base, size_t *bytes);
 int aqp_solver_connect(aqp_solver *s, void *const *peer_bases, int nranks);
-/* Optional, before aqp_solver_connect: the gather halos of every rank.  Rank
- * k gathers x only in [x_lohi[2k], x_lohi[2k+1]) (columns of its rows of A
- * and Q) and y only in [y_lohi[2k], y_lohi[2k+1]) (columns of its rows of
- * A'); producers then store to peer k only entries inside k's range.
- * Default: the whole vector (every peer gets everything). */
+/* Before aqp_solver_connect: the gather halos of every rank.  Rank k gathers
+ * x only in [x_lohi[2k], x_lohi[2k+1]) (columns of its rows of A and Q) and
+ * y only in [y_lohi[2k], y_lohi[2k+1]) (columns of its rows of A');
+ * producers store to peer k only entries inside k's range, which must lie
+ * inside k's gather window.  Default: the windows. */
 int aqp_solver_set_halos(aqp_solver *s, const int64_t *x_lohi, const int64_t *y_lohi, int nranks);
 /* x0 = clamp(0), y0 = 0, all round/anchor buffers <- (x0, y0) (engine.py:174-204) */
 int aqp_solver_init(aqp_solver *s, const aqp_scalars *sc);
@@ -277,7 +298,9 @@ int aqp_solver_restart(aqp_solver *s);        /* anchor, round start, z_prev <- 
 int aqp_solver_rollback(aqp_solver *s);       /* x, y, z_prev <- anchor; windows reset  */
 int aqp_solver_reset_window(aqp_solver *s);   /* zero window sums, forget avg_prev      */
 /* copy out: which: 0 = x_eval (box-projected x), 1 = y, 2 = dual slack r,
- * 3/4 = y-ray candidate 0/1, 5/6 = x-ray candidate 0/1 */
+ * 3/4 = y-ray candidate 0/1, 5/6 = x-ray candidate 0/1, 7 = x.  A row
+ * shard copies its own slice (len = n1-n0 or m1-m0); the host concatenates
+ * the ranks' slices in rank order. */
 int aqp_solver_read(aqp_solver *s, int which, double *host_out, int64_t len);
 /* launches_out[0]: kernels per outer iteration outside the BB loop;
  * launches_out[1]: kernels per BB iteration; launches_out[2]: 1 when the

@@ -22,9 +22,17 @@ c_double_p = C.POINTER(C.c_double)
 c_int64_p = C.POINTER(C.c_int64)
 
 
-class Shard(C.Structure):
+ABI_VERSION = 2
+
+
+class ShardDesc(C.Structure):
+    """aqp_shard_desc: this rank's rows, uploaded blocks and every rank's gather windows."""
+
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("n0", C.c_int64), ("n1", C.c_int64),
-                ("m0", C.c_int64), ("m1", C.c_int64)]
+                ("m0", C.c_int64), ("m1", C.c_int64), ("a_row0", C.c_int64), ("a_rows", C.c_int64),
+                ("q_row0", C.c_int64), ("a_local_nnz", C.c_int64), ("at_local_nnz", C.c_int64),
+                ("q_local_nnz", C.c_int64), ("xw", C.c_int64 * 16), ("yw", C.c_int64 * 16),
+                ("nl_cap", C.c_int64), ("ml_cap", C.c_int64)]
 
 
 class ProblemDesc(C.Structure):
@@ -40,6 +48,7 @@ class ProblemDesc(C.Structure):
         ("r_dense", C.c_int32), ("pad0_", C.c_int32),
         ("cost", C.c_void_p), ("var_lo", C.c_void_p), ("var_hi", C.c_void_p),
         ("con_lo", C.c_void_p), ("con_hi", C.c_void_p),
+        ("shard", C.c_void_p),
     ]
 
 
@@ -130,7 +139,6 @@ SIGNATURES = {
     "aqp_problem_scale": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P, C.c_size_t]),
     "aqp_solver_import_scaled": (C.c_int, [_P, _P, _P, _P]),
     # row shards (multi-GPU)
-    "aqp_problem_shard": (C.c_int, [_P, C.POINTER(Shard)]),
     "aqp_solver_exchange_region": (C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_size_t)]),
     "aqp_solver_connect": (C.c_int, [_P, C.POINTER(_P), C.c_int]),
     "aqp_solver_set_halos": (C.c_int, [_P, c_int64_p, c_int64_p, C.c_int]),
@@ -154,7 +162,7 @@ def load(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.aqp_abi_version() != 1:
+    if lib.aqp_abi_version() != ABI_VERSION:
         raise DeviceError("libaqp ABI version mismatch")
     _lib = lib
     return lib

@@ -84,18 +84,22 @@ def record_of(name: str, result) -> RunRecord:
                      r_dual=rep.r_dual, r_gap=rep.r_gap, objective=rep.primal_objective)
 
 
-_tls = threading.local()
+_pool_lock = threading.Lock()
+_stream_pool = {}  # (device, slot) -> torch stream, reused by every call
 
 
-def _thread_stream(device: int):
+def pooled_stream(device: int, slot: int):
+    """The process-wide stream of worker slot `slot` on `device`.  Solves on
+    one stream share one libaqp context (and its pinned staging), so reusing
+    the streams across calls bounds the contexts -- and the pinned host
+    memory -- to one per slot instead of one per call."""
     import torch
 
-    s = getattr(_tls, "stream", None)
-    if s is None or getattr(_tls, "device", None) != device:
-        torch.cuda.set_device(device)
-        s = _tls.stream = torch.cuda.Stream(device)
-        _tls.device = device
-    return s
+    with _pool_lock:
+        s = _stream_pool.get((device, slot))
+        if s is None:
+            s = _stream_pool[(device, slot)] = torch.cuda.Stream(device)
+        return s
 
 
 def solve_many(problems: Sequence, params: Optional[SolverParams] = None, streams: int = 8, device: int = 0,
@@ -115,11 +119,22 @@ def solve_many(problems: Sequence, params: Optional[SolverParams] = None, stream
     if streams == 1:
         return [solve(p, params, progress, device=device) for p in probs]
 
+    import queue
+
+    slots = queue.Queue()
+    for i in range(streams):
+        slots.put(i)
+
     def one(p):
-        with torch.cuda.stream(_thread_stream(device)):
-            r = solve(p, params, progress, device=device)
-            torch.cuda.current_stream().synchronize()
-            return r
+        slot = slots.get()  # a stream no other worker is using right now
+        try:
+            torch.cuda.set_device(device)
+            with torch.cuda.stream(pooled_stream(device, slot)):
+                r = solve(p, params, progress, device=device)
+                torch.cuda.current_stream().synchronize()
+                return r
+        finally:
+            slots.put(slot)
 
     with ThreadPoolExecutor(max_workers=streams) as pool:
         return list(pool.map(one, probs))

@@ -155,19 +155,25 @@ __device__ __forceinline__ void block_reduce(RedVals<NS, NM> &v, double *smem /*
 }
 
 // ---------------------------------------------------------------- row shards over peer memory
-// Multi-GPU: rank r owns rows [n0,n1) of A' and Q (x side)
-// and rows [m0,m1) of A (y side).  Every vector that an SpMV gathers is kept
-// full-length on every rank; the kernel that produces a rank's slice stores
-// it locally AND into the same offset of every peer's copy (NVLink P2P
-// stores into the peers' solver workspaces, whose exchange regions have the
-// identical layout on every rank, so peer address = local address +
-// delta[k]).  Reductions and barriers are one-block mailbox exchanges: each
-// rank writes its block-folded partials into mail[epoch & 1][rank] of every
-// peer, then releases flag[rank] = epoch on every peer and acquires all
-// flags >= epoch; every rank then combines the P partials in rank order, so
-// all ranks hold bitwise-identical scalars and take identical branches (the
-// CUDA-graph conditionals included).  No NCCL call sits on the data path.
+// Multi-GPU: rank r stores and owns rows [n0,n1) of A' and
+// Q (x side) and rows [m0,m1) of A (y side).  Every vector that an SpMV
+// gathers lives in a per-rank WINDOW [xw0, xw1) / [yw0, yw1) covering the
+// rank's own rows and every column its rows gather (column indices stay
+// global: a kernel gathers through base - xw0).  The kernel that produces a
+// rank's slice stores it locally AND into every peer's window that contains
+// the entry (NVLink P2P stores into the peers' solver workspaces; the
+// exchange regions have the identical layout on every rank -- buffers are
+// sized by max-over-ranks capacities -- so the peer address of entry g is
+// local address + delta[k] + 8 (xw0_self - xw0_k), precomputed per side as
+// xdelta / ydelta).  Reductions and barriers are one-block mailbox
+// exchanges: each rank writes its block-folded partials into
+// mail[epoch & 1][rank] of every peer, then releases flag[rank] = epoch on
+// every peer and acquires all flags >= epoch; every rank then combines the P
+// partials in rank order, so all ranks hold bitwise-identical scalars and
+// take identical branches (the CUDA-graph conditionals included).  No NCCL
+// call sits on the data path.
 constexpr int kMaxRanks = 8;
+constexpr int kMaxVec = 256;  // longest vector all-reduce (R x of a row-sharded low-rank Q)
 
 struct CommBlock {
   unsigned long long flag[kMaxRanks];  // flag[k]: last epoch rank k arrived at (written by rank k)
@@ -175,6 +181,7 @@ struct CommBlock {
   unsigned long long err;              // epoch of an exchange whose wait timed out (0 = none)
   unsigned long long pad[6];
   double mail[2][kMaxRanks][kMaxRed];
+  double vmail[2][kMaxRanks][kMaxVec];  // vector all-reduce (comm_allreduce_vec)
 };
 
 struct Comm {
@@ -182,11 +189,14 @@ struct Comm {
   CommBlock *cb = nullptr;
   unsigned long long timeout_ns = 30000000000ull;  // a peer that never arrives: give up, flag, carry on
   long long delta[kMaxRanks] = {};  // byte offset local -> rank k's mapping of the same buffer
+  // ... of an x-side / y-side gathered entry (the windows start at different
+  // global indices on different ranks): delta[k] + 8 (w0_self - w0_k)
+  long long xdelta[kMaxRanks] = {}, ydelta[kMaxRanks] = {};
   // Halo ranges: rank k only ever gathers x entries in [xlo[k], xhi[k]) (the
   // columns of its rows of A and Q) and y entries in [ylo[k], yhi[k]) (the
   // columns of its rows of A'), so a producer stores to peer k only what
   // falls in k's range -- for a banded C5 that is a boundary strip instead of
-  // the whole slice.  Defaults: everything.
+  // the whole slice.  Defaults: the windows.
   long long xlo[kMaxRanks] = {}, xhi[kMaxRanks] = {}, ylo[kMaxRanks] = {}, yhi[kMaxRanks] = {};
 };
 
@@ -204,22 +214,16 @@ __device__ __forceinline__ T *peer_addr(const Comm &c, T *p, int k) {
   return reinterpret_cast<T *>(reinterpret_cast<char *>(p) + peer_delta(c, k));
 }
 
-// store `val` at p[i] on every peer (the local store is the caller's)
-__device__ __forceinline__ void peer_put(const Comm &c, double *p, int64_t i, double val) {
-  if (c.nranks <= 1) return;
-#pragma unroll
-  for (int k = 0; k < kMaxRanks; ++k)
-    if (k < c.nranks && k != c.rank)
-      *reinterpret_cast<double *>(reinterpret_cast<char *>(p + i) + c.delta[k]) = val;
-}
-// ... only to the peers that gather global entry g (x side: side = 0, y side: 1)
+// store `val` (local entry p[i], global index g) into the window of every
+// peer that gathers g (x side: side = 0, y side: 1); the local store is the
+// caller's
 __device__ __forceinline__ void peer_put_halo(const Comm &c, int side, double *p, int64_t i, int64_t g, double val) {
   if (c.nranks <= 1) return;
 #pragma unroll
   for (int k = 0; k < kMaxRanks; ++k) {
     const long long lo = side ? c.ylo[k] : c.xlo[k], hi = side ? c.yhi[k] : c.xhi[k];
     if (k < c.nranks && k != c.rank && g >= lo && g < hi)
-      *reinterpret_cast<double *>(reinterpret_cast<char *>(p + i) + c.delta[k]) = val;
+      *reinterpret_cast<double *>(reinterpret_cast<char *>(p + i) + (side ? c.ydelta[k] : c.xdelta[k])) = val;
   }
 }
 
@@ -305,6 +309,47 @@ __device__ __forceinline__ void comm_allreduce(RedVals<NS, NM> &a, const Comm &c
     }
     __syncthreads();
   }
+}
+
+// Block-wide: in-place all-reduce (sum over ranks, combined in rank order)
+// of the `len` (<= kMaxVec) doubles at v; every thread of the block calls it.
+// All ranks end with bitwise-identical sums.  No-op for one rank.
+__device__ __forceinline__ void comm_allreduce_vec(double *v, int len, const Comm &c) {
+  if (c.nranks <= 1) return;
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) {
+    const unsigned long long e = c.cb->epoch + 1;
+    c.cb->epoch = e;
+    s_epoch = e;
+  }
+  __syncthreads();
+  const unsigned long long e = s_epoch;
+  const int P = c.nranks;
+  for (int t = threadIdx.x; t < P * len; t += blockDim.x) {
+    const int k = t / len, i = t % len;
+    *peer_addr(c, &c.cb->vmail[e & 1][c.rank][i], k) = v[i];
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < P) {
+    __threadfence_system();
+    st_release_sys(peer_addr(c, &c.cb->flag[c.rank], (int)threadIdx.x), e);
+    const unsigned long long t0 = global_ns_();
+    const bool broken = *(volatile unsigned long long *)&c.cb->err != 0;
+    while (!broken && ld_acquire_sys(&c.cb->flag[threadIdx.x]) < e) {
+      __nanosleep(64);
+      if (global_ns_() - t0 > c.timeout_ns) {
+        atomicCAS(&c.cb->err, 0ull, e);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    double a = __ldcv(&c.cb->vmail[e & 1][0][i]);
+    for (int k = 1; k < P; ++k) a += __ldcv(&c.cb->vmail[e & 1][k][i]);
+    v[i] = a;
+  }
+  __syncthreads();
 }
 
 // Grid-level epilogue: see grid_end / fin_op in aqp_kernels.cuh.

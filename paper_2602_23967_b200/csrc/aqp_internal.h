@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "aqp_common.cuh"
 
 // bump allocator over a caller-provided workspace; with base == nullptr it
@@ -20,6 +22,7 @@ struct CsrStore {
   int *ptr = nullptr;
   int *idx = nullptr;
   double *val = nullptr;
+  int64_t cap_nnz = 0;
   PlanItem *plan = nullptr;
   int64_t plan_cap = 0;
   double *seg_part = nullptr;
@@ -31,9 +34,10 @@ void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz);
 int upload_csr(aqp_ctx *ctx, CsrStore &s, DevCsr &M, int64_t rows, int64_t cols, const int64_t *d_ptr,
                const int64_t *d_idx, const double *d_val, int64_t nnz, const int64_t *host_ptr, bool strict,
                int *d_bad);
-int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool strict, Bump &scratch);
+int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool strict, Bump &scratch,
+                  int64_t col0 = 0, int64_t col1 = -1, int64_t row_base = 0, int64_t out_cols = -1);
 int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool strict, Bump &scratch,
-                   int64_t *nfull_out);
+                   int64_t *nfull_out, int64_t row_base = 0, int64_t r0 = 0, int64_t r1 = -1);
 size_t transpose_scratch_bytes(int64_t nnz, int64_t cols);
 size_t symmetrize_scratch_bytes(int64_t nnz, int64_t n);
 }  // namespace aqp
@@ -48,6 +52,10 @@ struct aqp_ctx {
   void *pinned = nullptr;
   void *bounce = nullptr;
   unsigned ring_i = 0;
+  // every solver call on this context holds it: solvers of one (device,
+  // stream) share the pinned control ring, pull block and bounce buffer, and
+  // host threads may call concurrently (ctypes releases the GIL)
+  std::recursive_mutex mu;
 };
 
 struct aqp_problem {
@@ -63,7 +71,14 @@ struct aqp_problem {
   int8_t *cone_r = nullptr, *recc_x = nullptr, *cone_y = nullptr, *recc_s = nullptr;
   int *bad = nullptr;
   aqp_problem_info info{};
-  // row shard (aqp_problem_shard): rows [n0,n1) of A' / Q, [m0,m1) of A
+  // row shard (aqp_shard_desc): this rank stores rows [n0,n1) of A' / Q and
+  // [m0,m1) of A only; gathered vectors live in the windows xwin / ywin
+  // (every rank's, [lo, hi) pairs), sized by the max-over-ranks capacities so
+  // the peer-visible solver layout is identical on every rank
   int rank = 0, nranks = 1;
   int64_t n0 = 0, n1 = 0, m0 = 0, m1 = 0;
+  int64_t xwin[2 * aqp::kMaxRanks] = {}, ywin[2 * aqp::kMaxRanks] = {};
+  int64_t nl_cap = 0, ml_cap = 0, xw_cap = 0, yw_cap = 0;
+  int64_t xw0() const { return xwin[2 * rank]; }
+  int64_t yw0() const { return ywin[2 * rank]; }
 };

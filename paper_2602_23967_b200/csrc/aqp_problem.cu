@@ -158,36 +158,58 @@ __global__ void k_hist(const int *__restrict__ keys, int64_t n, int *counts) {
     atomicAdd(counts + keys[i], 1);  // integer counts: order-independent
 }
 
-// transpose gather: out entry p comes from source entry src[p]
+// transpose keys restricted to the column window [col0, col1): an entry
+// outside it gets the sentinel key col1 - col0 (sorted last, then dropped)
+__global__ void k_tkeys(const int *__restrict__ idx, int64_t nnz, int col0, int col1, int *__restrict__ keys) {
+  const int sent = col1 - col0;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+    const int c = idx[k];
+    keys[k] = (c >= col0 && c < col1) ? c - col0 : sent;
+  }
+}
+
+// transpose gather: out entry p comes from source entry src[p]; its column
+// is the source row, offset by row_base (global row of a block's row 0)
 __global__ void k_gather_t(const int *__restrict__ src, const int *__restrict__ rid,
-                           const double *__restrict__ val, int64_t n, int *__restrict__ out_idx,
+                           const double *__restrict__ val, int64_t n, int row_base, int *__restrict__ out_idx,
                            double *__restrict__ out_val) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     const int k = src[p];
-    out_idx[p] = rid[k];
+    out_idx[p] = row_base + rid[k];
     out_val[p] = val[k];
   }
 }
 
-// full-symmetric expansion: combined entry list is
-//   [0, nnz)      mirrored copies (row = col_k, col = row_k), diagonal -> sentinel row n
+// ptr[i] = src[r0 + i] - src[r0] (a row window of a CSR, rebased)
+__global__ void k_rebase_ptr(const int *__restrict__ src, int64_t r0, int64_t rows, int *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= rows; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = src[r0 + i] - src[r0];
+}
+
+// full-symmetric expansion of an upper-triangle block whose row 0 is global
+// row `row_base`, restricted to the output rows [r0, r1); the combined entry
+// list is
+//   [0, nnz)      mirrored copies (row = col_k, col = row_k), diagonal -> sentinel
 //   [nnz, 2nnz)   the stored upper entries (row = row_k, col = col_k)
-__global__ void k_sym_keys(const int *__restrict__ rid, const int *__restrict__ col, int64_t nnz, int n,
-                           int *__restrict__ keys) {
+// with key = output row - r0, or the sentinel r1 - r0 for entries outside
+// the output rows (sorted last, then dropped).
+__global__ void k_sym_keys(const int *__restrict__ rid, const int *__restrict__ col, int64_t nnz, int row_base,
+                           int r0, int r1, int *__restrict__ keys) {
+  const int sent = r1 - r0;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-    const int r = rid[k], c = col[k];
-    keys[k] = (c == r) ? n : c;
-    keys[nnz + k] = r;
+    const int r = row_base + rid[k], c = col[k];
+    keys[k] = (c == r || c < r0 || c >= r1) ? sent : c - r0;
+    keys[nnz + k] = (r >= r0 && r < r1) ? r - r0 : sent;
   }
 }
 
 __global__ void k_sym_gather(const int *__restrict__ src, const int *__restrict__ rid,
                              const int *__restrict__ col, const double *__restrict__ val, int64_t nnz,
-                             int64_t nfull, int *__restrict__ out_idx, double *__restrict__ out_val) {
+                             int64_t nfull, int row_base, int *__restrict__ out_idx, double *__restrict__ out_val) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nfull; p += (int64_t)gridDim.x * blockDim.x) {
     const int s = src[p];
     if (s < nnz) {  // mirrored: column is the source row
-      out_idx[p] = rid[s];
+      out_idx[p] = row_base + rid[s];
       out_val[p] = val[s];
     } else {
       out_idx[p] = col[s - nnz];
@@ -306,24 +328,26 @@ static int build_sell(aqp_ctx *ctx, DevCsr &M, const P *hp) {
 }
 
 // ---------------------------------------------------------------- diagonal split (DevCsr::diag)
-__global__ void k_diag_pos(const int *__restrict__ ptr, const int *__restrict__ idx, int rows, int *missing) {
+// (global column of local row r's diagonal = r + row_off: a row shard's Q)
+__global__ void k_diag_pos(const int *__restrict__ ptr, const int *__restrict__ idx, int rows, int row_off,
+                           int *missing) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   bool found = false;
-  for (int k = ptr[r]; k < ptr[r + 1]; ++k) found |= idx[k] == r;
+  for (int k = ptr[r]; k < ptr[r + 1]; ++k) found |= idx[k] == r + row_off;
   if (!found) atomicAdd(missing, 1);
 }
 // row r loses exactly its diagonal entry: new ptr = old ptr - r
 __global__ void k_split_diag(const int *__restrict__ optr, const int *__restrict__ oidx,
-                             const double *__restrict__ oval, int rows, int *nptr, int *nidx, double *nval,
-                             double *diag) {
+                             const double *__restrict__ oval, int rows, int row_off, int *nptr, int *nidx,
+                             double *nval, double *diag) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r > rows) return;
   nptr[r] = optr[r] - r;
   if (r == rows) return;
   int w = optr[r] - r;
   for (int k = optr[r]; k < optr[r + 1]; ++k) {
-    if (oidx[k] == r) {
+    if (oidx[k] == r + row_off) {
       diag[r] = oval[k];
     } else {
       nidx[w] = oidx[k];
@@ -378,6 +402,7 @@ void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz) {
   s.ptr = (int *)b.take((rows + 1) * sizeof(int));
   s.idx = (int *)b.take(std::max<int64_t>(nnz, 1) * sizeof(int));
   s.val = (double *)b.take(std::max<int64_t>(nnz, 1) * sizeof(double));
+  s.cap_nnz = nnz;
   s.plan_cap = plan_capacity(rows, nnz);
   s.plan = (PlanItem *)b.take(s.plan_cap * sizeof(PlanItem));
   s.seg_cap = nnz / kSegNnz + nnz / kTileNnz + 2;  // each long row adds at most one partial segment
@@ -404,39 +429,63 @@ int upload_csr(aqp_ctx *ctx, CsrStore &s, DevCsr &M, int64_t rows, int64_t cols,
                      false);
 }
 
-// Transpose of an uploaded CSR (src) into storage t (rows = src.cols).
-// Scratch: rid(nnz) keys(nnz) keys2(nnz) vals(nnz) vals2(nnz) counts(cols+1) + cub.
-int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool strict, Bump &scratch) {
+// Transpose of an uploaded CSR (src) into storage t, restricted to the
+// source columns [col0, col1) (default: all): output row i is source column
+// col0 + i, its column indices are source rows + row_base (the global row of
+// the source's row 0; a row shard's A block), ascending -- a STABLE sort, so
+// the row-sequential product equals the Cython scatter order.  out_cols is
+// the output's column count (default: src.rows).
+// Scratch: rid(nnz) keys(nnz) keys2(nnz) vals(nnz) vals2(nnz) counts(rows_t+1) + cub.
+int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool strict, Bump &scratch, int64_t col0,
+                  int64_t col1, int64_t row_base, int64_t out_cols) {
   cudaStream_t st = ctx->stream;
   const int64_t nnz = src.nnz;
-  const int rows_t = src.cols;
+  if (col1 < 0) col1 = src.cols;
+  if (out_cols < 0) out_cols = src.rows;
+  const int rows_t = (int)(col1 - col0);
+  const bool window = col0 != 0 || col1 != src.cols;
   scratch.used = 0;
   int *rid = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
+  int *keys = window ? (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4) : nullptr;
   int *keys2 = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
   int *vals = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
   int *vals2 = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
-  int *counts = (int *)scratch.take((int64_t)(rows_t + 1) * 4);
-  size_t tb = sort_temp_bytes(std::max<int64_t>(nnz, rows_t + 1));
+  int *counts = (int *)scratch.take((int64_t)(rows_t + 2) * 4);
+  size_t tb = sort_temp_bytes(std::max<int64_t>(nnz, rows_t + 2));
   void *tmp = scratch.take(tb);
   if (scratch.overflow) return fail(AQP_ENOMEM, "transpose scratch too small");
-  AQP_CUDA(cudaMemsetAsync(counts, 0, (rows_t + 1) * sizeof(int), st));
+  AQP_CUDA(cudaMemsetAsync(counts, 0, (rows_t + 2) * sizeof(int), st));
+  int64_t nnz_t = nnz;
   if (nnz) {
+    const int *sort_keys = src.idx;
+    if (window) {
+      k_tkeys<<<setup_grid(nnz), 256, 0, st>>>(src.idx, nnz, (int)col0, (int)col1, keys);
+      sort_keys = keys;
+    }
     k_row_ids<<<setup_grid(src.rows), 256, 0, st>>>(src.ptr, src.rows, rid);
     k_iota<<<setup_grid(nnz), 256, 0, st>>>(vals, nnz);
-    k_hist<<<setup_grid(nnz), 256, 0, st>>>(src.idx, nnz, counts);
+    k_hist<<<setup_grid(nnz), 256, 0, st>>>(sort_keys, nnz, counts);  // counts[rows_t]: outside the window
     AQP_CUDA(cudaGetLastError());
     int end_bit = 1;
     while ((1LL << end_bit) <= (int64_t)rows_t) ++end_bit;
     size_t need = tb;
-    AQP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, src.idx, keys2, vals, vals2, (int)nnz, 0, end_bit, st));
-    k_gather_t<<<setup_grid(nnz), 256, 0, st>>>(vals2, rid, src.val, nnz, t.idx, t.val);
+    AQP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, sort_keys, keys2, vals, vals2, (int)nnz, 0, end_bit, st));
+    if (window) {
+      int outside = 0;
+      AQP_CUDA(cudaMemcpyAsync(&outside, counts + rows_t, sizeof(int), cudaMemcpyDeviceToHost, st));
+      AQP_CUDA(cudaStreamSynchronize(st));
+      nnz_t = nnz - outside;
+      AQP_CUDA(cudaMemsetAsync(counts + rows_t, 0, sizeof(int), st));
+    }
+    if (nnz_t > t.cap_nnz) return fail(AQP_ENOMEM, "transpose: more nonzeros than the storage holds");
+    k_gather_t<<<setup_grid(nnz_t), 256, 0, st>>>(vals2, rid, src.val, nnz_t, (int)row_base, t.idx, t.val);
     AQP_CUDA(cudaGetLastError());
   }
   AQP_TRY(counts_to_ptr(counts, rows_t, t.ptr, tmp, tb, st));
   AQP_CUDA(cudaMemsetAsync(t.seg_ticket, 0, t.seg_cap * sizeof(unsigned), st));
   T.rows = rows_t;
-  T.cols = src.rows;
-  T.nnz = nnz;
+  T.cols = (int)out_cols;
+  T.nnz = nnz_t;
   T.ptr = t.ptr;
   T.idx = t.idx;
   T.val = t.val;
@@ -447,12 +496,17 @@ int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool 
                      true);
 }
 
-// Full symmetric expansion of an uploaded upper-triangle CSR U (n x n).
+// Full symmetric expansion of an uploaded upper-triangle CSR U whose row 0 is
+// global row row_base (a row shard's P block; 0 for a whole n x n triangle),
+// restricted to the output rows [r0, r1) (default: all of U's rows).  Each
+// output row is [mirrored lower part | stored upper part], both ascending, in
+// global column indices.
 int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool strict, Bump &scratch,
-                   int64_t *nfull_out) {
+                   int64_t *nfull_out, int64_t row_base, int64_t r0, int64_t r1) {
   cudaStream_t st = ctx->stream;
   const int64_t nnz = U.nnz;
-  const int n = U.rows;
+  if (r1 < 0) r1 = U.rows;
+  const int n = (int)(r1 - r0);  // output rows
   const int64_t n2 = 2 * nnz;
   scratch.used = 0;
   int *rid = (int *)scratch.take(std::max<int64_t>(nnz, 1) * 4);
@@ -467,10 +521,10 @@ int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool s
   AQP_CUDA(cudaMemsetAsync(counts, 0, (n + 2) * sizeof(int), st));
   int64_t nfull = 0;
   if (nnz) {
-    k_row_ids<<<setup_grid(n), 256, 0, st>>>(U.ptr, n, rid);
-    k_sym_keys<<<setup_grid(nnz), 256, 0, st>>>(rid, U.idx, nnz, n, keys);
+    k_row_ids<<<setup_grid(U.rows), 256, 0, st>>>(U.ptr, U.rows, rid);
+    k_sym_keys<<<setup_grid(nnz), 256, 0, st>>>(rid, U.idx, nnz, (int)row_base, (int)r0, (int)r1, keys);
     k_iota<<<setup_grid(n2), 256, 0, st>>>(vals, n2);
-    k_hist<<<setup_grid(n2), 256, 0, st>>>(keys, n2, counts);  // counts[n] = #diagonal sentinels
+    k_hist<<<setup_grid(n2), 256, 0, st>>>(keys, n2, counts);  // counts[n] = #sentinels (diagonal mirrors, outside)
     AQP_CUDA(cudaGetLastError());
     int end_bit = 1;
     while ((1LL << end_bit) <= (int64_t)n) ++end_bit;
@@ -480,15 +534,18 @@ int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool s
     AQP_CUDA(cudaMemcpyAsync(&ndiag, counts + n, sizeof(int), cudaMemcpyDeviceToHost, st));
     AQP_CUDA(cudaStreamSynchronize(st));
     nfull = n2 - ndiag;
-    k_sym_gather<<<setup_grid(nfull), 256, 0, st>>>(vals2, rid, U.idx, U.val, nnz, nfull, f.idx, f.val);
+    if (nfull > f.cap_nnz) return fail(AQP_ENOMEM, "symmetrize: more nonzeros than the storage holds");
+    k_sym_gather<<<setup_grid(nfull), 256, 0, st>>>(vals2, rid, U.idx, U.val, nnz, nfull, (int)row_base, f.idx,
+                                                    f.val);
     AQP_CUDA(cudaGetLastError());
   }
   AQP_CUDA(cudaMemsetAsync(counts + n, 0, sizeof(int), st));
   AQP_TRY(counts_to_ptr(counts, n, f.ptr, tmp, tb, st));
   AQP_CUDA(cudaMemsetAsync(f.seg_ticket, 0, f.seg_cap * sizeof(unsigned), st));
   F.rows = n;
-  F.cols = n;
+  F.cols = U.cols;
   F.nnz = nfull;
+  F.row_off = (int)r0;
   F.ptr = f.ptr;
   F.idx = f.idx;
   F.val = f.val;
@@ -502,12 +559,9 @@ int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool s
 
 size_t transpose_scratch_bytes(int64_t nnz, int64_t cols) {
   Bump b;
-  b.take(std::max<int64_t>(nnz, 1) * 4);
-  b.take(std::max<int64_t>(nnz, 1) * 4);
-  b.take(std::max<int64_t>(nnz, 1) * 4);
-  b.take(std::max<int64_t>(nnz, 1) * 4);
-  b.take((cols + 1) * 4);
-  b.take(sort_temp_bytes(std::max<int64_t>(nnz, cols + 1)));
+  for (int i = 0; i < 5; ++i) b.take(std::max<int64_t>(nnz, 1) * 4);
+  b.take((cols + 2) * 4);
+  b.take(sort_temp_bytes(std::max<int64_t>(nnz, cols + 2)));
   return b.used + 256;
 }
 
@@ -583,7 +637,7 @@ static int split_q_diag(aqp_ctx *ctx, aqp_problem *p, Bump &scratch) {
   int *optr = (int *)scratch.take((int64_t)(n + 1) * 4);
   if (scratch.overflow) return AQP_OK;  // not enough scratch: keep the diagonal in the CSR
   AQP_CUDA(cudaMemsetAsync(missing, 0, 4, st));
-  k_diag_pos<<<(n + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, n, missing);
+  k_diag_pos<<<(n + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, n, M.row_off, missing);
   AQP_CUDA(cudaGetLastError());
   int miss = 0;
   AQP_CUDA(cudaMemcpyAsync(&miss, missing, 4, cudaMemcpyDeviceToHost, st));
@@ -593,7 +647,7 @@ static int split_q_diag(aqp_ctx *ctx, aqp_problem *p, Bump &scratch) {
   AQP_CUDA(cudaMemcpyAsync(oidx, M.idx, nnz * 4, cudaMemcpyDeviceToDevice, st));
   AQP_CUDA(cudaMemcpyAsync(oval, M.val, nnz * 8, cudaMemcpyDeviceToDevice, st));
   AQP_CUDA(cudaMemcpyAsync(optr, M.ptr, (int64_t)(n + 1) * 4, cudaMemcpyDeviceToDevice, st));
-  k_split_diag<<<(n + 256) / 256, 256, 0, st>>>(optr, oidx, oval, n, s.ptr, s.idx, s.val, p->qdiag);
+  k_split_diag<<<(n + 256) / 256, 256, 0, st>>>(optr, oidx, oval, n, M.row_off, s.ptr, s.idx, s.val, p->qdiag);
   AQP_CUDA(cudaGetLastError());
   std::vector<int> hptr((size_t)n + 1);
   AQP_CUDA(cudaMemcpyAsync(hptr.data(), s.ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -606,20 +660,47 @@ static int split_q_diag(aqp_ctx *ctx, aqp_problem *p, Bump &scratch) {
   return AQP_OK;
 }
 
+// persistent sizes: the whole problem, or (shard) this rank's rows only
+struct ProbDims {
+  int64_t nl, ml;        // local rows (x side, y side)
+  int64_t a_nnz, at_nnz;  // nonzeros stored for A and A'
+  int64_t q_nnz;         // capacity of the full symmetric Q rows
+  int64_t r_nnz;         // nonzeros of the (local) R
+};
+static ProbDims dims_of(const aqp_problem_desc *d) {
+  const aqp_shard_desc *sh = d->shard;
+  ProbDims g;
+  if (!sh) {
+    g.nl = d->n;
+    g.ml = d->m;
+    g.a_nnz = g.at_nnz = d->a_nnz;
+    g.q_nnz = 2 * d->q_nnz;
+  } else {
+    g.nl = sh->n1 - sh->n0;
+    g.ml = sh->m1 - sh->m0;
+    g.a_nnz = sh->a_local_nnz;
+    g.at_nnz = sh->at_local_nnz;
+    g.q_nnz = sh->q_local_nnz;
+  }
+  g.r_nnz = d->r_nnz;
+  return g;
+}
+
 static void layout_problem(Bump &b, const aqp_problem_desc *d, aqp_problem *p) {
-  const int64_t n = d->n, m = d->m;
-  layout_csr(b, p->sA, m, d->a_nnz);
-  layout_csr(b, p->sAt, n, d->a_nnz);
+  const ProbDims g = dims_of(d);
+  const int64_t n = g.nl, m = g.ml;
+  layout_csr(b, p->sA, m, g.a_nnz);
+  layout_csr(b, p->sAt, n, g.at_nnz);
   if (d->quad_kind != AQP_QUAD_DIAGONAL) {
-    layout_csr(b, p->sQ, n, 2 * d->q_nnz);
+    layout_csr(b, p->sQ, n, g.q_nnz);
     p->qdiag = (double *)b.take(std::max<int64_t>(n, 1) * 8);
   }
   if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
     if (d->r_dense) {
       p->sR.val = (double *)b.take(std::max<int64_t>(d->r_rows * n, 1) * 8);
     } else {
-      layout_csr(b, p->sR, d->r_rows, d->r_nnz);
-      layout_csr(b, p->sRt, n, d->r_nnz);
+      layout_csr(b, p->sR, d->r_rows, g.r_nnz);
+      layout_csr(b, p->sRt, n, g.r_nnz);
     }
   }
   p->c = (double *)b.take(std::max<int64_t>(n, 1) * 8);
@@ -635,21 +716,109 @@ static void layout_problem(Bump &b, const aqp_problem_desc *d, aqp_problem *p) {
   p->bad = (int *)b.take(64);
 }
 
+static int check_shard(const aqp_problem_desc *d) {
+  const aqp_shard_desc *sh = d->shard;
+  if (!sh) return AQP_OK;
+  if (sh->nranks < 1 || sh->nranks > kMaxRanks || sh->rank < 0 || sh->rank >= sh->nranks)
+    return fail(AQP_EINVAL, "rank / nranks out of range (at most 8 ranks)");
+  if (sh->n0 < 0 || sh->n1 > d->n || sh->n0 >= sh->n1 || sh->m0 < 0 || sh->m1 > d->m || sh->m0 >= sh->m1)
+    return fail(AQP_EINVAL, "shard row ranges must be non-empty and inside [0,n) / [0,m)");
+  if (sh->a_row0 < 0 || sh->a_rows < 0 || sh->a_row0 + sh->a_rows > d->m || sh->m0 < sh->a_row0 ||
+      sh->m1 > sh->a_row0 + sh->a_rows)
+    return fail(AQP_EINVAL, "the A block must cover the owned rows [m0,m1)");
+  if (d->quad_kind != AQP_QUAD_DIAGONAL && (sh->q_row0 < 0 || sh->q_row0 > sh->n0))
+    return fail(AQP_EINVAL, "the P block must start at or before n0");
+  if (sh->nl_cap < sh->n1 - sh->n0 || sh->ml_cap < sh->m1 - sh->m0) return fail(AQP_EINVAL, "row capacity too small");
+  for (int k = 0; k < sh->nranks; ++k)
+    if (sh->xw[2 * k] < 0 || sh->xw[2 * k + 1] > d->n || sh->xw[2 * k] > sh->xw[2 * k + 1] || sh->yw[2 * k] < 0 ||
+        sh->yw[2 * k + 1] > d->m || sh->yw[2 * k] > sh->yw[2 * k + 1])
+      return fail(AQP_EINVAL, "gather window outside [0,n) / [0,m)");
+  const int r = sh->rank;
+  if (sh->xw[2 * r] > sh->n0 || sh->xw[2 * r + 1] < sh->n1 || sh->yw[2 * r] > sh->m0 || sh->yw[2 * r + 1] < sh->m1)
+    return fail(AQP_EINVAL, "a rank's gather windows must cover its own rows");
+  if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && d->r_rows > kMaxVec)
+    return fail(AQP_EINVAL, "row-sharded low-rank Q supports at most 256 factor rows (R x is all-reduced)");
+  return AQP_OK;
+}
+
 int aqp_problem_sizes(const aqp_problem_desc *d, size_t *persistent_bytes, size_t *scratch_bytes) {
   AQP_TRY(check_desc(d));
+  AQP_TRY(check_shard(d));
   aqp_problem tmp;
   Bump b;
   layout_problem(b, d, &tmp);
-  size_t sc = transpose_scratch_bytes(d->a_nnz, d->n);
+  const aqp_shard_desc *sh = d->shard;
+  const ProbDims g = dims_of(d);
+  size_t sc;
+  if (!sh) {
+    sc = transpose_scratch_bytes(d->a_nnz, d->n);
+  } else {
+    // the int32 A block sits at the front of the scratch during its transpose
+    const size_t blk = (size_t)(sh->a_rows + 1) * 4 + (size_t)std::max<int64_t>(d->a_nnz, 1) * 4 + 1024;
+    sc = blk + transpose_scratch_bytes(d->a_nnz, g.nl);
+  }
   if (d->quad_kind != AQP_QUAD_DIAGONAL) {
-    // the int32 upper triangle sits at the front of the scratch during the expansion
-    const size_t up = (size_t)(d->n + 1) * 4 + (size_t)std::max<int64_t>(d->q_nnz, 1) * 12 + 1024;
-    sc = std::max(sc, up + symmetrize_scratch_bytes(d->q_nnz, d->n));
+    // the int32 upper triangle (block) sits at the front of the scratch during the expansion
+    const int64_t urows = sh ? sh->n1 - sh->q_row0 : d->n;
+    const size_t up = (size_t)(urows + 1) * 4 + (size_t)std::max<int64_t>(d->q_nnz, 1) * 12 + 1024;
+    sc = std::max(sc, up + symmetrize_scratch_bytes(d->q_nnz, g.nl));
   }
   if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && !d->r_dense)
-    sc = std::max(sc, transpose_scratch_bytes(d->r_nnz, d->n));
+    sc = std::max(sc, transpose_scratch_bytes(d->r_nnz, g.nl));
   if (persistent_bytes) *persistent_bytes = b.used + 256;
   if (scratch_bytes) *scratch_bytes = sc;
+  return AQP_OK;
+}
+
+// A row shard's A: rows [m0,m1) of the uploaded block, and A': the block's
+// columns [n0,n1) transposed (column indices = global rows of A).
+static int shard_a(aqp_ctx *ctx, aqp_problem *p, const aqp_problem_desc *d, const int64_t *host_ptr, void *scratch,
+                   size_t scratch_bytes) {
+  const aqp_shard_desc *sh = d->shard;
+  cudaStream_t st = ctx->stream;
+  Bump ub;
+  ub.base = scratch;
+  ub.cap = scratch_bytes;
+  int *bptr = (int *)ub.take((sh->a_rows + 1) * 4);
+  int *bidx = (int *)ub.take(std::max<int64_t>(d->a_nnz, 1) * 4);
+  if (ub.overflow) return fail(AQP_ENOMEM, "scratch too small for the A block");
+  AQP_TRY(to_i32(d->a_indptr, bptr, sh->a_rows + 1, INT32_MAX, p->bad, st));
+  AQP_TRY(to_i32(d->a_indices, bidx, d->a_nnz, d->n - 1, p->bad, st));
+  DevCsr B;
+  B.rows = (int)sh->a_rows;
+  B.cols = (int)d->n;
+  B.nnz = d->a_nnz;
+  B.ptr = bptr;
+  B.idx = bidx;
+  B.val = d->a_data;
+  // A = rows [m0, m1) of the block, copied (rebased) into its own storage
+  const int64_t r0 = sh->m0 - sh->a_row0, rows = sh->m1 - sh->m0;
+  const int64_t k0 = host_ptr[r0] - host_ptr[0], k1 = host_ptr[r0 + rows] - host_ptr[0];
+  if (k1 - k0 != sh->a_local_nnz) return fail(AQP_EINVAL, "a_local_nnz does not match the A block");
+  k_rebase_ptr<<<setup_grid(rows + 1), 256, 0, st>>>(bptr, r0, rows, p->sA.ptr);
+  AQP_CUDA(cudaGetLastError());
+  if (k1 > k0) {
+    AQP_CUDA(cudaMemcpyAsync(p->sA.idx, bidx + k0, (k1 - k0) * 4, cudaMemcpyDeviceToDevice, st));
+    AQP_CUDA(cudaMemcpyAsync(p->sA.val, d->a_data + k0, (k1 - k0) * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  AQP_CUDA(cudaMemsetAsync(p->sA.seg_ticket, 0, p->sA.seg_cap * sizeof(unsigned), st));
+  DevCsr &A = p->A;
+  A.rows = (int)rows;
+  A.cols = (int)d->n;
+  A.nnz = k1 - k0;
+  A.ptr = p->sA.ptr;
+  A.idx = p->sA.idx;
+  A.val = p->sA.val;
+  std::vector<int64_t> hp((size_t)rows + 1);
+  for (int64_t i = 0; i <= rows; ++i) hp[i] = host_ptr[r0 + i] - host_ptr[r0];
+  AQP_TRY(finish_plan(ctx, A, nullptr, hp.data(), false, p->sA.plan, p->sA.plan_cap, p->sA.seg_part,
+                      p->sA.seg_ticket, p->sA.seg_cap, false));
+  Bump rest;
+  const size_t used = (ub.used + 255) & ~size_t(255);
+  rest.base = static_cast<char *>(scratch) + used;
+  rest.cap = scratch_bytes - used;
+  AQP_TRY(transpose_csr(ctx, B, p->sAt, p->At, false, rest, sh->n0, sh->n1, sh->a_row0, d->m));
+  if (p->At.nnz != sh->at_local_nnz) return fail(AQP_EINVAL, "at_local_nnz does not match the A block");
   return AQP_OK;
 }
 
@@ -658,15 +827,43 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
                        size_t persistent_bytes, void *scratch, size_t scratch_bytes, aqp_problem **out) {
   (void)host_q_indptr;
   AQP_TRY(check_desc(d));
+  AQP_TRY(check_shard(d));
   if (!ctx || !out || !persistent || !host_a_indptr) return fail(AQP_EINVAL, "NULL argument");
   if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && !host_r_indptr) return fail(AQP_EINVAL, "R indptr missing");
   AQP_CUDA(cudaSetDevice(ctx->device));
+  const aqp_shard_desc *sh = d->shard;
+  const ProbDims g = dims_of(d);
   aqp_problem *p = new aqp_problem();
   p->ctx = ctx;
   p->n = d->n;
   p->m = d->m;
   p->n1 = d->n;
   p->m1 = d->m;
+  p->nl_cap = p->xw_cap = d->n;
+  p->ml_cap = p->yw_cap = d->m;
+  for (int k = 0; k < kMaxRanks; ++k) {
+    p->xwin[2 * k + 1] = d->n;
+    p->ywin[2 * k + 1] = d->m;
+  }
+  if (sh) {
+    p->rank = sh->rank;
+    p->nranks = sh->nranks;
+    p->n0 = sh->n0;
+    p->n1 = sh->n1;
+    p->m0 = sh->m0;
+    p->m1 = sh->m1;
+    p->nl_cap = sh->nl_cap;
+    p->ml_cap = sh->ml_cap;
+    p->xw_cap = p->yw_cap = 0;
+    for (int k = 0; k < 2 * kMaxRanks; ++k) {
+      p->xwin[k] = k < 2 * sh->nranks ? sh->xw[k] : 0;
+      p->ywin[k] = k < 2 * sh->nranks ? sh->yw[k] : 0;
+    }
+    for (int k = 0; k < sh->nranks; ++k) {
+      p->xw_cap = std::max(p->xw_cap, sh->xw[2 * k + 1] - sh->xw[2 * k]);
+      p->yw_cap = std::max(p->yw_cap, sh->yw[2 * k + 1] - sh->yw[2 * k]);
+    }
+  }
   p->quad_kind = d->quad_kind;
   Bump b;
   b.base = persistent;
@@ -682,38 +879,45 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
   cudaStream_t st = ctx->stream;
   int rc = AQP_OK;
   auto cleanup = [&](int code) {
+    for (DevCsr *M : {&p->A, &p->At, &p->Q, &p->R, &p->Rt}) free_sell(*M, st);
     delete p;
     return code;
   };
   AQP_CUDA(cudaMemsetAsync(p->bad, 0, 64, st));
-  rc = upload_csr(ctx, p->sA, p->A, d->m, d->n, d->a_indptr, d->a_indices, d->a_data, d->a_nnz, host_a_indptr,
-                  false, p->bad);
-  if (rc) return cleanup(rc);
-  rc = transpose_csr(ctx, p->A, p->sAt, p->At, false, sc);
+  if (!sh) {
+    rc = upload_csr(ctx, p->sA, p->A, d->m, d->n, d->a_indptr, d->a_indices, d->a_data, d->a_nnz, host_a_indptr,
+                    false, p->bad);
+    if (rc) return cleanup(rc);
+    rc = transpose_csr(ctx, p->A, p->sAt, p->At, false, sc);
+  } else {
+    rc = shard_a(ctx, p, d, host_a_indptr, scratch, scratch_bytes);
+  }
   if (rc) return cleanup(rc);
   p->q_full_nnz = 0;
-  const int64_t n = d->n, m = d->m;
+  const int64_t n = g.nl, m = g.ml;  // local rows
   if (d->quad_kind == AQP_QUAD_DIAGONAL) {
     if (n) AQP_CUDA(cudaMemcpyAsync(p->qd, d->q_values, n * 8, cudaMemcpyDeviceToDevice, st));
   } else {
-    // upload the upper triangle into the A' storage temporarily? no: into sQ's
-    // tail is unsafe; use the scratch-free path: upload to sQ, then expand via
-    // scratch copies of the upper arrays
+    // the upper triangle (a shard: its block of rows [q_row0, n1)) is
+    // converted to int32 at the front of the scratch, then expanded into
+    // the full symmetric rows this problem stores
+    const int64_t urow0 = sh ? sh->q_row0 : 0;
+    const int64_t urows = sh ? sh->n1 - sh->q_row0 : d->n;
     DevCsr U;
     CsrStore su;
-    Bump ub;  // the upper CSR lives in the first part of the scratch workspace
+    Bump ub;
     ub.base = scratch;
     ub.cap = scratch_bytes;
-    su.ptr = (int *)ub.take((n + 1) * 4);
+    su.ptr = (int *)ub.take((urows + 1) * 4);
     su.idx = (int *)ub.take(std::max<int64_t>(d->q_nnz, 1) * 4);
     su.val = (double *)ub.take(std::max<int64_t>(d->q_nnz, 1) * 8);
     if (ub.overflow) return cleanup(fail(AQP_ENOMEM, "scratch too small for Q upload"));
-    rc = to_i32(d->q_indptr, su.ptr, n + 1, INT32_MAX, p->bad, st);
-    if (!rc) rc = to_i32(d->q_indices, su.idx, d->q_nnz, n - 1, p->bad, st);
+    rc = to_i32(d->q_indptr, su.ptr, urows + 1, INT32_MAX, p->bad, st);
+    if (!rc) rc = to_i32(d->q_indices, su.idx, d->q_nnz, d->n - 1, p->bad, st);
     if (rc) return cleanup(rc);
     if (d->q_nnz) AQP_CUDA(cudaMemcpyAsync(su.val, d->q_data, d->q_nnz * 8, cudaMemcpyDeviceToDevice, st));
-    U.rows = (int)n;
-    U.cols = (int)n;
+    U.rows = (int)urows;
+    U.cols = (int)d->n;
     U.nnz = d->q_nnz;
     U.ptr = su.ptr;
     U.idx = su.idx;
@@ -721,13 +925,15 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
     Bump rest;
     rest.base = static_cast<char *>(scratch) + ((ub.used + 255) & ~size_t(255));
     rest.cap = scratch_bytes - ((ub.used + 255) & ~size_t(255));
-    rc = symmetrize_csr(ctx, U, p->sQ, p->Q, false, rest, &p->q_full_nnz);
+    rc = symmetrize_csr(ctx, U, p->sQ, p->Q, false, rest, &p->q_full_nnz, urow0, p->n0, p->n1);
     if (rc) return cleanup(rc);
+    if (sh && p->q_full_nnz != sh->q_local_nnz) return cleanup(fail(AQP_EINVAL, "q_local_nnz does not match the P block"));
     rc = split_q_diag(ctx, p, rest);
     if (rc) return cleanup(rc);
     if (n) AQP_CUDA(cudaMemcpyAsync(p->qd, d->q_diag, n * 8, cudaMemcpyDeviceToDevice, st));
     if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && d->r_dense) {
-      // full rows: the CSR values are R row-major; check the implied pattern
+      // full rows: the CSR values are R row-major (a shard: its columns
+      // [n0,n1) of every row); check the implied pattern
       for (int64_t i = 0; i <= d->r_rows; ++i)
         if (host_r_indptr[i] != i * n) return cleanup(fail(AQP_EINVAL, "r_dense set but R rows are not full"));
       if (d->r_nnz != d->r_rows * n) return cleanup(fail(AQP_EINVAL, "r_dense: r_nnz != r_rows * n"));
@@ -740,7 +946,8 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
     } else if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
       rc = upload_csr(ctx, p->sR, p->R, d->r_rows, d->n, d->r_indptr, d->r_indices, d->r_data, d->r_nnz,
                       host_r_indptr, false, p->bad);
-      if (!rc) rc = transpose_csr(ctx, p->R, p->sRt, p->Rt, false, sc);
+      if (!rc) rc = transpose_csr(ctx, p->R, p->sRt, p->Rt, false, sc, p->n0, p->n1, 0, d->r_rows);
+      if (!rc && p->Rt.nnz != d->r_nnz) rc = fail(AQP_EINVAL, "R block has columns outside [n0,n1)");
       if (rc) return cleanup(rc);
     }
   }
@@ -761,7 +968,7 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
   AQP_CUDA(cudaStreamSynchronize(st));
   if (bad) return cleanup(fail(AQP_EINVAL, "index out of range in CSR upload"));
   std::memset(&p->info, 0, sizeof(p->info));
-  p->info.a_nnz = d->a_nnz;
+  p->info.a_nnz = p->A.nnz;
   p->info.at_nnz = p->At.nnz;
   p->info.q_full_nnz = p->q_full_nnz;
   p->info.r_rows = d->r_rows;
@@ -772,50 +979,6 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
   p->info.q_items = p->Q.nitems;
   p->info.persistent_bytes = b.used;
   *out = p;
-  return AQP_OK;
-}
-
-// Restrict the SpMV passes to rows [r0, r1) of M: the row pointers are a
-// window of the full array (absolute nonzero offsets, so idx/val stay put)
-// and the work plan is rebuilt for the local rows.
-static int slice_rows(aqp_ctx *ctx, DevCsr &M, CsrStore &s, int64_t r0, int64_t r1, int row_off, bool may_stage) {
-  std::vector<int> hptr((size_t)(r1 - r0 + 1));
-  AQP_CUDA(cudaMemcpyAsync(hptr.data(), M.ptr + r0, hptr.size() * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  AQP_CUDA(cudaStreamSynchronize(ctx->stream));
-  M.ptr += r0;
-  if (M.diag) M.diag += r0;
-  M.rows = (int)(r1 - r0);
-  M.nnz = (int64_t)hptr.back() - hptr.front();
-  M.row_off = row_off;
-  AQP_CUDA(cudaMemsetAsync(s.seg_ticket, 0, s.seg_cap * sizeof(unsigned), ctx->stream));
-  return finish_plan(ctx, M, hptr.data(), nullptr, false, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap,
-                     may_stage);
-}
-
-int aqp_problem_shard(aqp_problem *p, const aqp_shard *sh) {
-  if (!p || !sh) return fail(AQP_EINVAL, "NULL argument");
-  if (p->nranks > 1 || p->n0 || p->m0 || p->n1 != p->n || p->m1 != p->m)
-    return fail(AQP_ESTATE, "problem is already sharded");
-  if (sh->nranks < 1 || sh->nranks > kMaxRanks || sh->rank < 0 || sh->rank >= sh->nranks)
-    return fail(AQP_EINVAL, "rank / nranks out of range (at most 8 ranks)");
-  if (sh->n0 < 0 || sh->n1 > p->n || sh->n0 >= sh->n1 || sh->m0 < 0 || sh->m1 > p->m || sh->m0 >= sh->m1)
-    return fail(AQP_EINVAL, "shard row ranges must be non-empty and inside [0,n) / [0,m)");
-  if (sh->nranks > 1 && p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK)
-    return fail(AQP_EINVAL, "low-rank Q is not row-sharded (R x needs every column)");
-  AQP_CUDA(cudaSetDevice(p->ctx->device));
-  AQP_TRY(slice_rows(p->ctx, p->A, p->sA, sh->m0, sh->m1, 0, false));
-  AQP_TRY(slice_rows(p->ctx, p->At, p->sAt, sh->n0, sh->n1, 0, true));
-  if (p->quad_kind == AQP_QUAD_SPARSE)
-    AQP_TRY(slice_rows(p->ctx, p->Q, p->sQ, sh->n0, sh->n1, (int)sh->n0, false));
-  p->rank = sh->rank;
-  p->nranks = sh->nranks;
-  p->n0 = sh->n0;
-  p->n1 = sh->n1;
-  p->m0 = sh->m0;
-  p->m1 = sh->m1;
-  p->info.a_items = p->A.nitems;
-  p->info.at_items = p->At.nitems;
-  p->info.q_items = p->Q.nitems;
   return AQP_OK;
 }
 

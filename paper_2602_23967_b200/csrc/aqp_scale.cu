@@ -93,16 +93,32 @@ __global__ void k_diag_norm(const double *__restrict__ q, const double *__restri
   if (i < n) out[i] = fabs(q[i]) * D[i] * D[i];
 }
 // a split-out diagonal of Q (DevCsr::diag) joins the row norm / is scaled by D^2
-__global__ void k_add_diag_norm(double *__restrict__ nrm, const double *__restrict__ q, const double *__restrict__ D,
-                                int64_t n, int l1) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double v = fabs(q[i]) * D[i] * D[i];
-  nrm[i] = l1 ? nrm[i] + v : fmax(nrm[i], v);
+// row norms of a full symmetric Q whose diagonal is split out of the CSR
+// (DevCsr::diag): the diagonal term enters at its column position, so the l1
+// sums are bitwise those of the unsplit CSR (AQP_SPLIT_DIAG=0)
+__global__ void k_row_norm_split(DevCsr M, const double *__restrict__ D, int l1, double *__restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= M.rows) return;
+  const int gr = r + M.row_off;
+  const double s = D[r];
+  const double dv = fabs(M.diag[r]) * s * D[r];
+  double a = 0.0;
+  bool done = false;
+  for (int k = M.ptr[r]; k < M.ptr[r + 1]; ++k) {
+    if (!done && M.idx[k] > gr) {
+      a = l1 ? a + dv : fmax(a, dv);
+      done = true;
+    }
+    const double v = fabs(M.val[k]) * s * D[M.idx[k]];
+    a = l1 ? a + v : fmax(a, v);
+  }
+  if (!done) a = l1 ? a + dv : fmax(a, dv);
+  out[r] = a;
 }
+// q = (q * d) * d: the order k_scale_csr applies to a CSR diagonal entry
 __global__ void k_scale_diag(double *q, const double *D, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) q[i] *= D[i] * D[i];
+  if (i < n) q[i] = q[i] * D[i] * D[i];
 }
 __global__ void k_fill(double *p, int64_t n, double v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -134,8 +150,10 @@ int aqp_problem_scale(aqp_problem *p, int ruiz_iters, int pock_chambolle, double
     // x side: A' rows (= A columns) with row scale D, col scale E
     if (n) k_row_norm<<<grid_of(n), 256, 0, st>>>(p->At, D, E, l1, nx1);
     if (sparse_q && n) {
-      k_row_norm<<<grid_of(n), 256, 0, st>>>(p->Q, D, D, l1, nx2);  // full symmetric P: rows = columns
-      if (p->Q.diag) k_add_diag_norm<<<grid_of(n), 256, 0, st>>>(nx2, p->Q.diag, D, n, l1);
+      if (p->Q.diag)  // full symmetric P: rows = columns
+        k_row_norm_split<<<grid_of(n), 256, 0, st>>>(p->Q, D, l1, nx2);
+      else
+        k_row_norm<<<grid_of(n), 256, 0, st>>>(p->Q, D, D, l1, nx2);
     } else if (n) {
       k_diag_norm<<<grid_of(n), 256, 0, st>>>(p->qd, D, n, nx2);    // diagonal Q: |q_j| d_j^2
     }

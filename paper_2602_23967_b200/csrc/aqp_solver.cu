@@ -83,6 +83,7 @@ struct SV {
   // row shards: vector pointers above are offset to this rank's slice
   // (x side by xoff, y side by yoff); gathers index the full copies
   int64_t xoff, yoff, nl, ml;
+  int pair_ok;  // the BB step's slices are 16-byte aligned: paired (128-bit) step kernel
   Comm cm;
   cudaGraphConditionalHandle bb_cond, outer_cond;
   int in_graph;  // 0 for stand-alone launches (kernel timing): no conditional updates
@@ -560,7 +561,6 @@ struct OpRtv {
 // order), R'(Rx) is a streaming pass whose entry i sums k products in row
 // order -- bitwise the order of the reference's csr_matvec_t over R
 // (_core.pyx:45-59).  Both read R once: 8 k n bytes per pass.
-#ifndef AQP_DENSE_RX_V1
 // R x, every warp on every row: a block owns kRxCols columns; warp w owns the
 // column slice [w*S, (w+1)*S) (S = kRxCols / kWarps) of the chunk and walks
 // all k rows over it (coalesced 128-bit loads of R, x from shared memory),
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_rx(SV v, int src) {
   pdl_wait();
   if (lowrank_skip(v, src)) return;
   const double *x = lowrank_src(v, src);
-  const int64_t n = v.n;
+  const int64_t n = v.nl;  // this rank's columns of R (all of them unsharded)
   const int64_t j0 = (int64_t)blockIdx.x * kRxCols;
   const int len = (int)min((int64_t)kRxCols, n - j0);
   for (int t = threadIdx.x; t < kRxCols; t += kThreads) xs[t] = t < len ? x[j0 + t] : 0.0;
@@ -636,64 +636,6 @@ __global__ void __launch_bounds__(kThreads) k_dense_rx(SV v, int src) {
   pdl_trigger();
 }
 
-#else
-constexpr int kRxCols = 4096;  // columns per block of the R x pass (32 KB of x in smem)
-inline int64_t dense_rx_blocks(int64_t n) { return std::max<int64_t>((n + kRxCols - 1) / kRxCols, 1); }
-__device__ __forceinline__ bool cand_valid(const Ctrl *ct, int j, double norm);
-
-__device__ __forceinline__ const double *lowrank_src(const SV &v, int src) {
-  const Ctrl *ct = v.ctrl;
-  return src == 0 ? pick3(v.xbb, 0) : src == 1 ? pick3(v.xbb, ct->bb_new) : src == 2 ? v.xeval : pick2(v.dx, src - 3);
-}
-// x-ray candidates only when the cheap test passed (certify.py:148-157)
-__device__ __forceinline__ bool lowrank_skip(const SV &v, int src) {
-  if (src < 3) return false;
-  const Ctrl *ct = v.ctrl;
-  const int j = src - 3;
-  const double *xr = ct->red + R_XR + 5 * j;
-  return !(cand_valid(ct, j, xr[0]) && xr[1] < -v.eps_tol);
-}
-
-__global__ void __launch_bounds__(kThreads) k_dense_rx(SV v, int src) {
-  __shared__ __align__(16) double xs[kRxCols];
-  pdl_wait();
-  if (lowrank_skip(v, src)) return;
-  const double *x = lowrank_src(v, src);
-  const int64_t n = v.n;
-  const int64_t j0 = (int64_t)blockIdx.x * kRxCols;
-  const int len = (int)min((int64_t)kRxCols, n - j0);
-  for (int t = threadIdx.x; t < len; t += kThreads) xs[t] = x[j0 + t];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool vec = (n & 1) == 0;  // rows 16-byte aligned
-  for (int kk = warp; kk < v.rk; kk += kWarps) {
-    const double *row = v.Rd + (int64_t)kk * n + j0;
-    double a0 = 0.0, a1 = 0.0;
-    if (vec) {
-      const double2 *r2 = reinterpret_cast<const double2 *>(row);
-      const double2 *x2 = reinterpret_cast<const double2 *>(xs);
-      const int h = len >> 1;
-#pragma unroll 4
-      for (int u = lane; u < h; u += 32) {
-        const double2 r = __ldcs(r2 + u);  // streamed once per pass: do not keep in L2
-        const double2 q = x2[u];
-        a0 += r.x * q.x;
-        a1 += r.y * q.y;
-      }
-      if ((len & 1) && lane == 0) a0 += row[len - 1] * xs[len - 1];
-    } else {
-#pragma unroll 4
-      for (int u = lane; u < len; u += 32) a0 += __ldcs(row + u) * xs[u];
-    }
-    double a = a0 + a1;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-    if (lane == 0) v.rxpart[(size_t)kk * gridDim.x + blockIdx.x] = a;
-  }
-  pdl_trigger();
-}
-
-#endif
 
 // rx[k] = fold of the k-th row's block partials (block order, fixed tree)
 __global__ void __launch_bounds__(kThreads) k_dense_rx_fold(SV v, int src, int nb) {
@@ -709,6 +651,23 @@ __global__ void __launch_bounds__(kThreads) k_dense_rx_fold(SV v, int src, int n
   if (threadIdx.x == 0) v.rx[kk] = a.s[0];
 }
 
+// Row shards: R x over this rank's columns is a partial sum; all-reduce the
+// k values over the ranks (rank order, bitwise-identical on every rank)
+// before R'(R x).  One block.
+__global__ void __launch_bounds__(kThreads) k_rx_allreduce(SV v, int src) {
+  __shared__ double buf[kMaxVec];
+  pdl_wait();
+  if (lowrank_skip(v, src)) {  // identical decision on every rank (all-reduced scalars)
+    pdl_trigger();
+    return;
+  }
+  for (int i = threadIdx.x; i < v.rk; i += blockDim.x) buf[i] = v.rx[i];
+  __syncthreads();
+  comm_allreduce_vec(buf, v.rk, v.cm);
+  for (int i = threadIdx.x; i < v.rk; i += blockDim.x) v.rx[i] = buf[i];
+  pdl_trigger();  // after the wait: see the scheduling rule in DESIGN.md §6
+}
+
 // rtv[i] = sum_k R[k, i] rx[k], k ascending
 __global__ void __launch_bounds__(kThreads) k_dense_rtv(SV v, int src) {
   __shared__ double rxs[1024];
@@ -717,7 +676,7 @@ __global__ void __launch_bounds__(kThreads) k_dense_rtv(SV v, int src) {
   const int k = v.rk;
   for (int t = threadIdx.x; t < k && t < 1024; t += kThreads) rxs[t] = v.rx[t];
   __syncthreads();
-  const int64_t n = v.n;
+  const int64_t n = v.nl;
   for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
     double s = 0.0;
 #pragma unroll 8
@@ -1098,20 +1057,17 @@ struct OpPush {
       case 4: p = v.dx[0]; break;
       case 5: p = v.dx[1]; break;
       case 6: p = pick3(v.xbb, 1); break;
-      case 7: p = v.tm; break;
-      case 8: p = v.rs; break;
-      default: p = pick3(v.xs, ct->xcur); break;
+      default: p = v.tm; break;
     }
   }
-  int full;  // replicate everything (vectors read back by the host), else the gather halos
   int side;  // 0: x side, 1: y side
   __device__ void elem(int64_t i, RedVals<0, 0> &) const {
-    if (full) peer_put(v.cm, p, i, p[i]);
-    else peer_put_halo(v.cm, side, p, i, i + (side ? v.yoff : v.xoff), p[i]);
+    peer_put_halo(v.cm, side, p, i, i + (side ? v.yoff : v.xoff), p[i]);
   }
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
-enum PushBuf : int { PB_Y = 0, PB_XEVAL, PB_DY0, PB_DY1, PB_DX0, PB_DX1, PB_PW, PB_TM, PB_RS, PB_X };
+// gathered (windowed) buffers only: a push stores this rank's slice into the peers' windows
+enum PushBuf : int { PB_Y = 0, PB_XEVAL, PB_DY0, PB_DY1, PB_DX0, PB_DX1, PB_PW, PB_TM };
 
 // ---------------------------------------------------------------- scaled solves
 // Certification of a scaled solve (aqp_problem_scale) on the ORIGINAL
@@ -1240,6 +1196,9 @@ __global__ void __cluster_dims__(kFoldCtas, 1, 1) __launch_bounds__(kFoldThreads
   __shared__ double swarp[NW * (NT > 0 ? NT : 1)];
   cg::cluster_group cl = cg::this_cluster();
   const unsigned crank = cl.block_rank();
+  // DSMEM stores into CTA 0 need it to have started: arrive now, wait just
+  // before the remote stores (the partials loads overlap the barrier)
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   pdl_wait();
   const bool shard = g.comm.nranks > 1;
   if (!shard) pdl_trigger();
@@ -1282,6 +1241,7 @@ __global__ void __cluster_dims__(kFoldCtas, 1, 1) __launch_bounds__(kFoldThreads
 #pragma unroll
       for (int i = 0; i < NM; ++i) a.m[i] = nanmax(a.m[i], __shfl_xor_sync(0xffffffffu, a.m[i], off));
     }
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (lane == 0) {
       double *dst = cl.map_shared_rank(swarp, 0);
       const int vw = (int)crank * (kFoldThreads / 32) + warp;
@@ -1290,6 +1250,8 @@ __global__ void __cluster_dims__(kFoldCtas, 1, 1) __launch_bounds__(kFoldThreads
 #pragma unroll
       for (int i = 0; i < NM; ++i) dst[vw * NT + NS + i] = a.m[i];
     }
+  } else {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
   cl.sync();  // every CTA's warp totals are in CTA 0
   if (crank != 0) return;
@@ -1362,34 +1324,40 @@ struct aqp_solver {
 namespace {
 
 void layout_solver(Bump &b, aqp_problem *p, SV &v, Ctrl **ctrl, GridRed &gr) {
-  const int64_t n = std::max<int64_t>(p->n, 1), m = std::max<int64_t>(p->m, 1);
+  // gathered vectors: one gather window each (the whole vector unsharded);
+  // the others: this rank's rows.  Sizes are max-over-ranks capacities, so
+  // every offset below is the same on every rank.
+  const int64_t xw = std::max<int64_t>(p->xw_cap, 1), yw = std::max<int64_t>(p->yw_cap, 1);
+  const int64_t n = std::max<int64_t>(p->nl_cap, 1), m = std::max<int64_t>(p->ml_cap, 1);
+  auto vxw = [&]() { return (double *)b.take(xw * 8); };
+  auto vyw = [&]() { return (double *)b.take(yw * 8); };
   auto vn = [&]() { return (double *)b.take(n * 8); };
   auto vm = [&]() { return (double *)b.take(m * 8); };
   for (int i = 0; i < 3; ++i) v.xs[i] = vn();
-  for (int i = 0; i < 3; ++i) v.ys[i] = vm();
+  for (int i = 0; i < 3; ++i) v.ys[i] = vyw();
   v.anc_x = vn(); v.anc_y = vm();
   v.xlast = vn(); v.ylast = vm();
   v.xblk = vn(); v.yblk = vm();
   v.xavgp = vn(); v.yavgp = vm();
-  v.lin = vn(); v.xbar = vn();
-  for (int i = 0; i < 3; ++i) v.xbb[i] = vn();
+  v.lin = vn(); v.xbar = vxw();
+  for (int i = 0; i < 3; ++i) v.xbb[i] = vxw();
   for (int i = 0; i < 2; ++i) v.gbb[i] = vn();
   v.rx = (double *)b.take(std::max<int64_t>(p->R.rows, 1) * 8);
   v.rtv = vn();
-  v.xeval = vn(); v.qx = vn(); v.aty = vn(); v.rs = vn();
-  v.dx[0] = vn(); v.dx[1] = vn();
-  v.dy[0] = vm(); v.dy[1] = vm();
-  v.tm = vm();
+  v.xeval = vxw(); v.qx = vn(); v.aty = vn(); v.rs = vn();
+  v.dx[0] = vxw(); v.dx[1] = vxw();
+  v.dy[0] = vyw(); v.dy[1] = vyw();
+  v.tm = vyw();
   *ctrl = (Ctrl *)b.take(sizeof(Ctrl));
-  // everything above has the same offsets on every rank (sizes depend on the
-  // global n, m only): the peer-visible exchange region.  Partials below are
-  // sized by this rank's plan.
+  // everything above (and the comm block) has the same offsets on every
+  // rank: the peer-visible exchange region.  Partials below are sized by this
+  // rank's plan.
   gr.comm.cb = (CommBlock *)b.take(sizeof(CommBlock));
   int64_t maxg = 148 * 8;
   for (const DevCsr *M : {&p->A, &p->At, &p->Q, &p->R, &p->Rt}) maxg = std::max<int64_t>(maxg, M->nitems);
   gr.partials = (double *)b.take(maxg * kMaxRed * 8);
   gr.ticket = (unsigned *)b.take(64);  // [0] grid_end ticket
-  if (p->r_dense) v.rxpart = (double *)b.take(std::max<int64_t>(p->R.rows, 1) * dense_rx_blocks(p->n) * 8);
+  if (p->r_dense) v.rxpart = (double *)b.take(std::max<int64_t>(p->R.rows, 1) * dense_rx_blocks(p->R.cols) * 8);
 }
 
 // explicit graph construction helpers
@@ -1520,20 +1488,41 @@ cudaError_t run_elem_fin(cudaStream_t st, int64_t n, const Op &op, GridRed gr) {
 }
 
 // stream launch of the dense R x / R'(R x) passes (eager windows, checks)
-int dense_lowrank(aqp_solver *s, int src) {
+// stream launch of Q's low-rank part R'(R x) for source `src` (lowrank_src);
+// row shards all-reduce the partial R x between the two passes
+int run_lowrank(aqp_solver *s, int src) {
   aqp_problem *p = s->p;
   cudaStream_t st = p->ctx->stream;
-  const int nb = (int)dense_rx_blocks(p->n);
-  k_dense_rx<<<nb, kThreads, 0, st>>>(s->v, src);
-  k_dense_rx_fold<<<p->R.rows, kThreads, 0, st>>>(s->v, src, nb);
-  k_dense_rtv<<<elem_grid(p->n), kThreads, 0, st>>>(s->v, src);
+  SV v = s->v;
+  v.in_graph = 0;
+  if (p->r_dense) {
+    const int nb = (int)dense_rx_blocks(p->R.cols);
+    k_dense_rx<<<nb, kThreads, 0, st>>>(v, src);
+    k_dense_rx_fold<<<p->R.rows, kThreads, 0, st>>>(v, src, nb);
+  } else if (src >= 3) {
+    OpXRayRx rx{}; rx.v = v; rx.src = src; rx.j = src - 3;
+    AQP_CUDA(run_spmv(st, p->R, rx, s->gr));
+  } else {
+    OpRx rx{}; rx.v = v; rx.src = src;
+    AQP_CUDA(run_spmv(st, p->R, rx, s->gr));
+  }
+  if (s->shard) k_rx_allreduce<<<1, kThreads, 0, st>>>(v, src);
+  if (p->r_dense) {
+    k_dense_rtv<<<elem_grid(p->R.cols), kThreads, 0, st>>>(v, src);
+  } else if (src >= 3) {
+    OpXRayRtv rt{}; rt.v = v; rt.src = src; rt.j = src - 3;
+    AQP_CUDA(run_spmv(st, p->Rt, rt, s->gr));
+  } else {
+    OpRtv rt{}; rt.v = v; rt.src = src;
+    AQP_CUDA(run_spmv(st, p->Rt, rt, s->gr));
+  }
   AQP_CUDA(cudaGetLastError());
   return AQP_OK;
 }
 
 // stream launch of the BB step (paired 128-bit kernel when the slice is aligned)
 int run_step(cudaStream_t st, const SV &v, const OpStep &o, GridRed gr) {
-  if ((v.xoff & 1) == 0)
+  if (v.pair_ok)
     k_step2<<<elem_grid(std::max<int64_t>(v.nl / 2, 1)), kThreads, 0, st>>>(v.nl, o, gr);
   else
     elem_op<OpStep><<<elem_grid(v.nl), kThreads, 0, st>>>(v.nl, o, gr);
@@ -1543,23 +1532,24 @@ int run_step(cudaStream_t st, const SV &v, const OpStep &o, GridRed gr) {
 
 int add_lowrank(aqp_solver *s, cudaGraph_t g, GNode &last, int src) {
   aqp_problem *p = s->p;
+  SV v = s->v;
+  v.in_graph = 1;
   if (p->r_dense) {
-    SV v = s->v;
-    v.in_graph = 1;
-    const int nb = (int)dense_rx_blocks(p->n);
+    const int nb = (int)dense_rx_blocks(p->R.cols);
     AQP_CUDA(add_node(g, last, (unsigned)nb, k_dense_rx, v, src));
     AQP_CUDA(add_node(g, last, (unsigned)p->R.rows, k_dense_rx_fold, v, src, nb));
-    AQP_CUDA(add_node(g, last, (unsigned)elem_grid(p->n), k_dense_rtv, v, src));
+    if (s->shard) AQP_CUDA(add_node(g, last, 1u, k_rx_allreduce, v, src));
+    AQP_CUDA(add_node(g, last, (unsigned)elem_grid(p->R.cols), k_dense_rtv, v, src));
     return AQP_OK;
   }
   OpRx rx{};
-  rx.v = s->v;
-  rx.v.in_graph = 1;
+  rx.v = v;
   rx.src = src;
   OpRtv rt{};
-  rt.v = rx.v;
+  rt.v = v;
   rt.src = src;
   AQP_CUDA(node_spmv(g, last, p->R, rx, s->gr));
+  if (s->shard) AQP_CUDA(add_node(g, last, 1u, k_rx_allreduce, v, src));
   AQP_CUDA(node_spmv(g, last, p->Rt, rt, s->gr));
   return AQP_OK;
 }
@@ -1633,7 +1623,7 @@ int build_graph(aqp_solver *s) {
       OpStep st{};
       st.v = v;
       st.cond = u > 0;
-      if ((v.xoff & 1) == 0)  // 16-byte aligned slices: the paired (128-bit) step
+      if (v.pair_ok)  // 16-byte aligned slices: the paired (128-bit) step
         AQP_CUDA(add_node(ib, il, (unsigned)elem_grid(std::max<int64_t>(v.nl / 2, 1)), k_step2, v.nl, st, gr));
       else
         AQP_CUDA(node_elem(ib, il, v.nl, st, gr));
@@ -1725,14 +1715,13 @@ int pull_ctrl(aqp_solver *s) {
 
 // row shards: replicate this rank's slice of buffer `which` (PushBuf) into
 // the peers' copies and wait until every rank has done the same
-int push_buf(aqp_solver *s, int which, bool full = false) {
+int push_buf(aqp_solver *s, int which) {
   if (!s->shard) return AQP_OK;
   cudaStream_t st = s->p->ctx->stream;
   const bool yside = which == PB_Y || which == PB_DY0 || which == PB_DY1 || which == PB_TM;
   OpPush o{};
   o.v = s->v;
   o.which = which;
-  o.full = full ? 1 : 0;
   o.side = yside ? 1 : 0;
   AQP_CUDA(run_elem(st, yside ? s->v.ml : s->v.nl, o, s->gr));
   k_comm_barrier<<<1, 32, 0, st>>>(s->gr);
@@ -1802,36 +1791,41 @@ int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, si
   v.rk = p->R.rows;
   v.n = p->n;
   v.m = p->m;
-  // row shards (aqp_problem_shard): offset every vector to this rank's slice
+  // row shards (aqp_shard_desc): vectors of this rank's rows start at its
+  // row 0; gathered vectors (windows starting at global xw0 / yw0) point at
+  // the rank's own slice inside the window, so `ptr - xoff + global column`
+  // addresses the window and every local row r is `ptr[r]`
   v.xoff = p->n0;
   v.yoff = p->m0;
   v.nl = p->n1 - p->n0;
   v.ml = p->m1 - p->m0;
   s->ws_base = ws;
   s->shard = p->nranks > 1;
-  if (!p->ctx->pinned) {
-    AQP_CUDA(cudaMallocHost(&p->ctx->pinned, sizeof(aqp_solver::Pinned)));
-    AQP_CUDA(cudaMallocHost(&p->ctx->bounce, aqp_solver::kBounce * 8));
+  {
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (!p->ctx->pinned) {
+      AQP_CUDA(cudaMallocHost(&p->ctx->pinned, sizeof(aqp_solver::Pinned)));
+      AQP_CUDA(cudaMallocHost(&p->ctx->bounce, aqp_solver::kBounce * 8));
+    }
   }
   s->pin = static_cast<aqp_solver::Pinned *>(p->ctx->pinned);
   s->bounce = static_cast<double *>(p->ctx->bounce);
-  if (p->n0 || p->m0) {
-    for (int i = 0; i < 3; ++i) { v.xs[i] += v.xoff; v.ys[i] += v.yoff; v.xbb[i] += v.xoff; }
-    for (int i = 0; i < 2; ++i) { v.gbb[i] += v.xoff; v.dx[i] += v.xoff; v.dy[i] += v.yoff; }
-    for (double **q : {&v.anc_x, &v.xlast, &v.xblk, &v.xavgp, &v.lin, &v.xbar, &v.rtv, &v.xeval, &v.qx, &v.aty, &v.rs})
-      *q += v.xoff;
-    for (double **q : {&v.anc_y, &v.ylast, &v.yblk, &v.yavgp, &v.tm}) *q += v.yoff;
-    v.c += v.xoff; v.vlo += v.xoff; v.vhi += v.xoff; v.qd += v.xoff;
-    v.cone_r += v.xoff; v.recc_x += v.xoff;
-    v.clo += v.yoff; v.chi += v.yoff; v.cone_y += v.yoff; v.recc_s += v.yoff;
+  {
+    const int64_t gx = p->n0 - p->xw0(), gy = p->m0 - p->yw0();
+    for (int i = 0; i < 3; ++i) { v.ys[i] += gy; v.xbb[i] += gx; }
+    for (int i = 0; i < 2; ++i) { v.dx[i] += gx; v.dy[i] += gy; }
+    v.xbar += gx;
+    v.xeval += gx;
+    v.tm += gy;
+    v.pair_ok = (gx & 1) == 0;  // x_t / x slots sit gx entries into 256-byte aligned windows
   }
   s->gr.comm.rank = p->rank;
   s->gr.comm.nranks = 1;  // until aqp_solver_connect
-  for (int k = 0; k < kMaxRanks; ++k) {
-    s->gr.comm.xlo[k] = 0;
-    s->gr.comm.xhi[k] = p->n;
-    s->gr.comm.ylo[k] = 0;
-    s->gr.comm.yhi[k] = p->m;
+  for (int k = 0; k < kMaxRanks; ++k) {  // default halos: the gather windows
+    s->gr.comm.xlo[k] = p->xwin[2 * k];
+    s->gr.comm.xhi[k] = p->xwin[2 * k + 1];
+    s->gr.comm.ylo[k] = p->ywin[2 * k];
+    s->gr.comm.yhi[k] = p->ywin[2 * k + 1];
   }
   v.cm = s->gr.comm;
   std::memset(&s->h, 0, sizeof(Ctrl));
@@ -1867,6 +1861,7 @@ int aqp_solver_import_scaled(aqp_solver *dst, aqp_solver *src, const double *D, 
   if (!dst || !src || !D || !E) return fail(AQP_EINVAL, "NULL argument");
   if (dst->p->n != src->p->n || dst->p->m != src->p->m || dst->shard || src->shard)
     return fail(AQP_EINVAL, "import needs two unsharded solvers of the same shape");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(dst->p->ctx->mu);
   cudaStream_t st = dst->p->ctx->stream;
   if (src->p->ctx->stream != st) AQP_CUDA(cudaStreamSynchronize(src->p->ctx->stream));
   const int64_t big = std::max(dst->p->n, dst->p->m);
@@ -1887,9 +1882,12 @@ int aqp_solver_set_halos(aqp_solver *s, const int64_t *x_lohi, const int64_t *y_
   if (!s || !x_lohi || !y_lohi) return fail(AQP_EINVAL, "NULL argument");
   if (nranks != s->p->nranks || nranks > kMaxRanks) return fail(AQP_EINVAL, "nranks differs from the problem's shard");
   if (s->exec) return fail(AQP_ESTATE, "set the halos before aqp_solver_connect");
+  const aqp_problem *p = s->p;
   for (int k = 0; k < nranks; ++k) {
-    if (x_lohi[2 * k] < 0 || x_lohi[2 * k + 1] > s->p->n || y_lohi[2 * k] < 0 || y_lohi[2 * k + 1] > s->p->m)
-      return fail(AQP_EINVAL, "halo range outside [0,n) / [0,m)");
+    const bool xe = x_lohi[2 * k] >= x_lohi[2 * k + 1], ye = y_lohi[2 * k] >= y_lohi[2 * k + 1];
+    if ((!xe && (x_lohi[2 * k] < p->xwin[2 * k] || x_lohi[2 * k + 1] > p->xwin[2 * k + 1])) ||
+        (!ye && (y_lohi[2 * k] < p->ywin[2 * k] || y_lohi[2 * k + 1] > p->ywin[2 * k + 1])))
+      return fail(AQP_EINVAL, "halo range outside the rank's gather window");
     s->gr.comm.xlo[k] = x_lohi[2 * k];
     s->gr.comm.xhi[k] = x_lohi[2 * k + 1];
     s->gr.comm.ylo[k] = y_lohi[2 * k];
@@ -1901,6 +1899,7 @@ int aqp_solver_set_halos(aqp_solver *s, const int64_t *x_lohi, const int64_t *y_
 
 int aqp_solver_connect(aqp_solver *s, void *const *peer_bases, int nranks) {
   if (!s || !peer_bases) return fail(AQP_EINVAL, "NULL argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   aqp_problem *p = s->p;
   if (nranks != p->nranks) return fail(AQP_EINVAL, "nranks differs from the problem's shard");
   if (nranks == 1) return peer_bases[0] == s->ws_base ? AQP_OK : fail(AQP_EINVAL, "peer_bases[0] is not this workspace");
@@ -1908,10 +1907,13 @@ int aqp_solver_connect(aqp_solver *s, void *const *peer_bases, int nranks) {
   Comm c = s->gr.comm;
   c.nranks = nranks;
   if (const char *t = getenv("AQP_COMM_TIMEOUT_S")) c.timeout_ns = (unsigned long long)(atof(t) * 1e9);
-  for (int k = 0; k < kMaxRanks; ++k) c.delta[k] = 0;
+  for (int k = 0; k < kMaxRanks; ++k) c.delta[k] = c.xdelta[k] = c.ydelta[k] = 0;
   for (int k = 0; k < nranks; ++k) {
     if (!peer_bases[k]) return fail(AQP_EINVAL, "NULL peer base");
     c.delta[k] = (long long)((const char *)peer_bases[k] - (const char *)s->ws_base);
+    // entry g sits at window offset g - w0 on every rank
+    c.xdelta[k] = c.delta[k] + 8 * (long long)(p->xw0() - p->xwin[2 * k]);
+    c.ydelta[k] = c.delta[k] + 8 * (long long)(p->yw0() - p->ywin[2 * k]);
   }
   if (c.delta[p->rank] != 0) return fail(AQP_EINVAL, "peer_bases[rank] must be this solver's workspace");
   AQP_CUDA(cudaSetDevice(p->ctx->device));
@@ -1956,6 +1958,7 @@ int aqp_solver_destroy(aqp_solver *s) {
 
 int aqp_solver_init(aqp_solver *s, const aqp_scalars *sc) {
   if (!s || !sc) return fail(AQP_EINVAL, "NULL argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   s->h.s = *sc;
   s->h.xcur = 0; s->h.xprev = 1; s->h.ycur = 0; s->h.yprev = 1;
   s->h.pw_stop = 0;
@@ -1966,12 +1969,14 @@ int aqp_solver_init(aqp_solver *s, const aqp_scalars *sc) {
 
 int aqp_solver_set_scalars(aqp_solver *s, const aqp_scalars *sc) {
   if (!s || !sc) return fail(AQP_EINVAL, "NULL argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   s->h.s = *sc;
   return push_scalars(s);
 }
 
 int aqp_solver_get_scalars(aqp_solver *s, aqp_scalars *sc) {
   if (!s || !sc) return fail(AQP_EINVAL, "NULL argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   AQP_TRY(pull_ctrl(s));
   *sc = s->h.s;
   return AQP_OK;
@@ -1989,18 +1994,7 @@ static int run_eager(aqp_solver *s, int64_t n_iters) {
   GridRed gr = s->gr;
   const bool diag = p->quad_kind == AQP_QUAD_DIAGONAL;
   const bool lowrank = p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK;
-  auto lowrank_pass = [&](int src) -> int {
-    if (p->r_dense) return dense_lowrank(s, src);
-    OpRx rx{};
-    rx.v = v;
-    rx.src = src;
-    OpRtv rt{};
-    rt.v = v;
-    rt.src = src;
-    AQP_CUDA(run_spmv(st, p->R, rx, gr));
-    AQP_CUDA(run_spmv(st, p->Rt, rt, gr));
-    return AQP_OK;
-  };
+  auto lowrank_pass = [&](int src) -> int { return run_lowrank(s, src); };
   for (int64_t it = 0; it < n_iters; ++it) {
     if (diag) {
       OpP1Diag o{};
@@ -2052,6 +2046,7 @@ static int run_eager(aqp_solver *s, int64_t n_iters) {
 
 int aqp_solver_run(aqp_solver *s, int64_t n_iters) {
   if (!s) return fail(AQP_EINVAL, "NULL argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   if (!s->exec && !s->eager) return fail(AQP_ESTATE, "sharded solver is not connected (aqp_solver_connect)");
   if (n_iters <= 0) return AQP_OK;
   // host mirror is current (the host only changes scalars between windows)
@@ -2066,6 +2061,7 @@ int aqp_solver_run(aqp_solver *s, int64_t n_iters) {
 
 int aqp_solver_check(aqp_solver *s, int with_rays, aqp_check_result *out) {
   if (!s || !out) return fail(AQP_EINVAL, "NULL argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   aqp_problem *p = s->p;
   cudaStream_t st = p->ctx->stream;
   const SV &v = s->v;
@@ -2081,14 +2077,7 @@ int aqp_solver_check(aqp_solver *s, int with_rays, aqp_check_result *out) {
     AQP_TRY(push_buf(s, PB_DY1));
   }
   if (p->quad_kind != AQP_QUAD_DIAGONAL) {
-    if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && p->r_dense) {
-      AQP_TRY(dense_lowrank(s, 2));
-    } else if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
-      OpRx rx{}; rx.v = v; rx.src = 2;
-      OpRtv rt{}; rt.v = v; rt.src = 2;
-      AQP_CUDA(run_spmv(st, p->R, rx, gr));
-      AQP_CUDA(run_spmv(st, p->Rt, rt, gr));
-    }
+    if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) AQP_TRY(run_lowrank(s, 2));
     OpStoreT<true> q{}; q.v = v; q.src = 0; q.dst = 0; q.red = -1;
     AQP_CUDA(run_spmv(st, p->Q, q, gr));
   }
@@ -2108,14 +2097,7 @@ int aqp_solver_check(aqp_solver *s, int with_rays, aqp_check_result *out) {
         OpChkXRayT<false> q{}; q.v = v; q.j = j; q.which = 1;
         AQP_CUDA(run_elem(st, v.nl, q, gr));
       } else {
-        if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && p->r_dense) {
-          AQP_TRY(dense_lowrank(s, 3 + j));
-        } else if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) {
-          OpXRayRx rx{}; rx.v = v; rx.src = 3 + j; rx.j = j;
-          OpXRayRtv rt{}; rt.v = v; rt.src = 3 + j; rt.j = j;
-          AQP_CUDA(run_spmv(st, p->R, rx, gr));
-          AQP_CUDA(run_spmv(st, p->Rt, rt, gr));
-        }
+        if (p->quad_kind == AQP_QUAD_SPARSE_LOW_RANK) AQP_TRY(run_lowrank(s, 3 + j));
         OpChkXRayT<true> q{}; q.v = v; q.j = j; q.which = 1;
         AQP_CUDA(run_spmv(st, p->Q, q, gr));
       }
@@ -2154,30 +2136,38 @@ int aqp_solver_check(aqp_solver *s, int with_rays, aqp_check_result *out) {
   return AQP_OK;
 }
 
-int aqp_solver_mark_cert(aqp_solver *s) { return s ? state_op(s, 1) : fail(AQP_EINVAL, "NULL"); }
-int aqp_solver_restart(aqp_solver *s) { return s ? state_op(s, 2) : fail(AQP_EINVAL, "NULL"); }
-int aqp_solver_rollback(aqp_solver *s) { return s ? state_op(s, 3) : fail(AQP_EINVAL, "NULL"); }
+static int locked_state_op(aqp_solver *s, int mode) {
+  if (!s) return fail(AQP_EINVAL, "NULL");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
+  return state_op(s, mode);
+}
+int aqp_solver_mark_cert(aqp_solver *s) { return locked_state_op(s, 1); }
+int aqp_solver_restart(aqp_solver *s) { return locked_state_op(s, 2); }
+int aqp_solver_rollback(aqp_solver *s) { return locked_state_op(s, 3); }
 
 int aqp_solver_reset_window(aqp_solver *s) {
   if (!s) return fail(AQP_EINVAL, "NULL");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   AQP_TRY(state_op(s, 4));
   return AQP_OK;
 }
 
 int aqp_solver_read(aqp_solver *s, int which, double *host_out, int64_t len) {
   if (!s || !host_out) return fail(AQP_EINVAL, "NULL argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   const SV &v = s->v;
   const double *src = nullptr;
+  const int64_t nx = v.nl, ny = v.ml;  // a row shard copies its own slice
   int64_t need = 0;
   switch (which) {
-    case 0: src = v.xeval; need = s->p->n; break;
-    case 1: src = pick3(v.ys, s->h.ycur); need = s->p->m; break;
-    case 2: src = v.rs; need = s->p->n; break;
-    case 3: src = pick2(v.dy, 0); need = s->p->m; break;
-    case 4: src = pick2(v.dy, 1); need = s->p->m; break;
-    case 5: src = pick2(v.dx, 0); need = s->p->n; break;
-    case 6: src = pick2(v.dx, 1); need = s->p->n; break;
-    case 7: src = pick3(v.xs, s->h.xcur); need = s->p->n; break;
+    case 0: src = v.xeval; need = nx; break;
+    case 1: src = pick3(v.ys, s->h.ycur); need = ny; break;
+    case 2: src = v.rs; need = nx; break;
+    case 3: src = pick2(v.dy, 0); need = ny; break;
+    case 4: src = pick2(v.dy, 1); need = ny; break;
+    case 5: src = pick2(v.dx, 0); need = nx; break;
+    case 6: src = pick2(v.dx, 1); need = nx; break;
+    case 7: src = pick3(v.xs, s->h.xcur); need = nx; break;
     default: return fail(AQP_EINVAL, "unknown buffer id");
   }
   if (len != need) return fail(AQP_EINVAL, "length mismatch");
@@ -2185,13 +2175,6 @@ int aqp_solver_read(aqp_solver *s, int which, double *host_out, int64_t len) {
     AQP_TRY(pull_ctrl(s));
     src = which == 1 ? pick3(v.ys, s->h.ycur) : pick3(v.xs, s->h.xcur);
   }
-  const bool yside = which == 1 || which == 3 || which == 4;
-  if (s->shard) {
-    // collective: every rank replicates its slice, then reads the full vector
-    static const int kPush[8] = {PB_XEVAL, PB_Y, PB_RS, PB_DY0, PB_DY1, PB_DX0, PB_DX1, PB_X};
-    AQP_TRY(push_buf(s, kPush[which], true));
-  }
-  src -= yside ? v.yoff : v.xoff;
   cudaStream_t st = s->p->ctx->stream;
   for (int64_t off = 0; off < need; off += (int64_t)aqp_solver::kBounce) {  // via the pinned bounce buffer
     const int64_t len = std::min<int64_t>(need - off, (int64_t)aqp_solver::kBounce);
@@ -2216,6 +2199,7 @@ int aqp_solver_counters(aqp_solver *s, int64_t *out) {
 // power iteration for the step size (linalg.py:287-312); runs before init
 int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, double *out, int *annihilated) {
   if (!s || !host_v0 || !out || !annihilated) return fail(AQP_EINVAL, "NULL argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   aqp_problem *p = s->p;
   cudaStream_t st = p->ctx->stream;
   const SV &v = s->v;
@@ -2223,12 +2207,15 @@ int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, do
   const int64_t n = v.nl;
   *annihilated = 0;
   AQP_TRY(poke(s, &Ctrl::pw_stop, 0));
-  // every rank holds the whole start vector (drawn on the host): copy it whole
-  for (int64_t off = 0; off < p->n; off += (int64_t)aqp_solver::kBounce) {
-    const int64_t len = std::min<int64_t>(p->n - off, (int64_t)aqp_solver::kBounce);
+  // every rank holds the whole start vector (drawn on the host): copy its
+  // gather window (the whole vector unsharded)
+  const int64_t w0 = p->xwin[2 * p->rank], w1 = p->xwin[2 * p->rank + 1];
+  double *win = pick3(v.xbb, 0) - v.xoff + w0;
+  for (int64_t off = 0; off < w1 - w0; off += (int64_t)aqp_solver::kBounce) {
+    const int64_t len = std::min<int64_t>(w1 - w0 - off, (int64_t)aqp_solver::kBounce);
     AQP_CUDA(cudaStreamSynchronize(st));  // the bounce buffer is free again
-    std::memcpy(s->bounce, host_v0 + off, len * 8);
-    AQP_CUDA(cudaMemcpyAsync(pick3(v.xbb, 0) - v.xoff + off, s->bounce, len * 8, cudaMemcpyHostToDevice, st));
+    std::memcpy(s->bounce, host_v0 + w0 + off, len * 8);
+    AQP_CUDA(cudaMemcpyAsync(win + off, s->bounce, len * 8, cudaMemcpyHostToDevice, st));
   }
   // nv = |v|; u = v / nv; |A u| > 0 ?
   { OpPwNorm o{}; o.v = v; o.idx = 0; o.slot = R_PW; AQP_CUDA(run_elem(st, n, o, gr)); }
@@ -2282,6 +2269,7 @@ __global__ void k_flush_read(const double2 *p, int64_t n2, double *sink) {
 // BB fields, so re-init before solving.
 int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, size_t flush_bytes, double *avg_ms) {
   if (!s || !avg_ms || reps <= 0) return fail(AQP_EINVAL, "bad argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   aqp_problem *p = s->p;
   cudaStream_t st = p->ctx->stream;
   SV v = s->v;
@@ -2348,7 +2336,7 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
       }
       case 6: {  // dense R x (block partials + fold), source x_t
         if (!p->r_dense) return fail(AQP_EINVAL, "kernel 6 needs a dense low-rank R");
-        const int nb = (int)dense_rx_blocks(p->n);
+        const int nb = (int)dense_rx_blocks(p->R.cols);
         k_dense_rx<<<nb, kThreads, 0, st>>>(v, 1);
         k_dense_rx_fold<<<p->R.rows, kThreads, 0, st>>>(v, 1, nb);
         AQP_CUDA(cudaGetLastError());
@@ -2356,7 +2344,7 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
       }
       case 7: {  // dense R'(R x)
         if (!p->r_dense) return fail(AQP_EINVAL, "kernel 7 needs a dense low-rank R");
-        k_dense_rtv<<<elem_grid(p->n), kThreads, 0, st>>>(v, 1);
+        k_dense_rtv<<<elem_grid(p->R.cols), kThreads, 0, st>>>(v, 1);
         AQP_CUDA(cudaGetLastError());
         break;
       }
@@ -2418,6 +2406,7 @@ int aqp_ipc_close(void *dev_ptr, size_t offset) {
 // first, and resets the ring; *count = pairs copied (0 when tracing is off).
 int aqp_solver_trace(aqp_solver *s, unsigned long long *host_out, int64_t cap, int64_t *count) {
   if (!s || !count) return fail(AQP_EINVAL, "NULL argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock_(s->p->ctx->mu);
   *count = 0;
   if (!s->gr.trace) return AQP_OK;
   cudaStream_t st = s->p->ctx->stream;

@@ -77,9 +77,12 @@ def _full_rows(r) -> bool:
 
 
 class DeviceProblem:
-    """HBM copy of one QpProblem (reference model.py:124-165)."""
+    """HBM copy of one QpProblem (reference model.py:124-165), or -- with
+    ``part`` (shard.LocalPart) -- of one rank's row shard of it: only that
+    rank's rows of A, A' and Q and its entries of the vectors are uploaded
+    and stored (aqp_shard_desc)."""
 
-    def __init__(self, problem: QpProblem, ctx: DeviceContext = None):
+    def __init__(self, problem: QpProblem, ctx: DeviceContext = None, part=None):
         self.ctx = ctx or DeviceContext.get()
         lib = self.ctx.lib
         p = problem
@@ -94,35 +97,66 @@ class DeviceProblem:
 
         d = nat.ProblemDesc()
         d.n, d.m = p.n, p.m
-        d.a_indptr, d.a_indices, d.a_data, d.a_nnz = up(a.indptr), up(a.indices), up(a.data), a.nnz
+        sh = None
+        if part is None:
+            a_ptr, a_idx, a_val = a.indptr, a.indices, a.data
+        else:
+            a_ptr, a_idx, a_val = part.a_indptr, part.a_indices, part.a_data
+        d.a_indptr, d.a_indices, d.a_data, d.a_nnz = up(a_ptr), up(a_idx), up(a_val), len(a_val)
         host_q = host_r = None
         if q.kind == "diagonal":
             d.quad_kind = nat.QUAD_DIAGONAL
-            d.q_values = up(q.values)
+            d.q_values = up(q.values if part is None else part.q_vec)
         else:
             pq = q if q.kind == "sparse" else q.p
             d.quad_kind = nat.QUAD_SPARSE if q.kind == "sparse" else nat.QUAD_SPARSE_LOW_RANK
-            d.q_indptr, d.q_indices, d.q_data = up(pq.upper.indptr), up(pq.upper.indices), up(pq.upper.data)
-            d.q_nnz = pq.upper.nnz
-            d.q_diag = up(pq.diag)
-            host_q = pq.upper.indptr
+            if part is None:
+                q_ptr, q_idx, q_val, q_diag = pq.upper.indptr, pq.upper.indices, pq.upper.data, pq.diag
+            else:
+                q_ptr, q_idx, q_val, q_diag = part.q_indptr, part.q_indices, part.q_data, part.q_vec
+            d.q_indptr, d.q_indices, d.q_data = up(q_ptr), up(q_idx), up(q_val)
+            d.q_nnz = len(q_val)
+            d.q_diag = up(q_diag)
+            host_q = np.ascontiguousarray(q_ptr, dtype=np.int64)
             if q.kind == "sparse_low_rank":
                 r = q.r
                 d.r_rows = r.rows
-                d.r_dense = int(_full_rows(r))
-                d.r_indptr = up(r.indptr)
-                d.r_indices = 0 if d.r_dense else up(r.indices)  # dense: the indices are implied
-                d.r_data, d.r_nnz = up(r.data), r.nnz
-                host_r = r.indptr
-        d.cost, d.var_lo, d.var_hi = up(p.cost), up(p.var_bounds.lower), up(p.var_bounds.upper)
-        d.con_lo, d.con_hi = up(p.con_bounds.lower), up(p.con_bounds.upper)
+                if part is None:
+                    d.r_dense = int(_full_rows(r))
+                    r_ptr, r_idx, r_val = r.indptr, r.indices, r.data
+                else:
+                    d.r_dense = int(part.r_dense)
+                    r_ptr, r_idx, r_val = part.r_indptr, part.r_indices, part.r_data
+                d.r_indptr = up(r_ptr)
+                d.r_indices = 0 if d.r_dense else up(r_idx)  # dense: the indices are implied
+                d.r_data, d.r_nnz = up(r_val), len(r_val)
+                host_r = np.ascontiguousarray(r_ptr, dtype=np.int64)
+        src = p if part is None else None
+        d.cost = up(p.cost if src else part.cost)
+        d.var_lo = up(p.var_bounds.lower if src else part.var_lo)
+        d.var_hi = up(p.var_bounds.upper if src else part.var_hi)
+        d.con_lo = up(p.con_bounds.lower if src else part.con_lo)
+        d.con_hi = up(p.con_bounds.upper if src else part.con_hi)
+        if part is not None:
+            me = part.me
+            sh = nat.ShardDesc(rank=me.rank, nranks=me.nranks, n0=me.n0, n1=me.n1, m0=me.m0, m1=me.m1,
+                               a_row0=me.ywin[0], a_rows=me.ywin[1] - me.ywin[0], q_row0=me.q_row0,
+                               a_local_nnz=me.a_local_nnz, at_local_nnz=me.at_local_nnz,
+                               q_local_nnz=me.q_local_nnz,
+                               nl_cap=max(pl.n1 - pl.n0 for pl in part.plans),
+                               ml_cap=max(pl.m1 - pl.m0 for pl in part.plans))
+            for k, pl in enumerate(part.plans):
+                sh.xw[2 * k], sh.xw[2 * k + 1] = pl.xwin
+                sh.yw[2 * k], sh.yw[2 * k + 1] = pl.ywin
+            d.shard = C.addressof(sh)
+        host_a = np.ascontiguousarray(a_ptr, dtype=np.int64)
         pb, sb = C.c_size_t(), C.c_size_t()
         nat.check(lib.aqp_problem_sizes(C.byref(d), C.byref(pb), C.byref(sb)), "aqp_problem_sizes")
         self.workspace = self.ctx.empty(pb.value)
         scratch = self.ctx.empty(sb.value)
         h = C.c_void_p()
         rc = lib.aqp_problem_create(
-            self.ctx.handle, C.byref(d), a.indptr.ctypes.data,
+            self.ctx.handle, C.byref(d), host_a.ctypes.data,
             None if host_q is None else host_q.ctypes.data,
             None if host_r is None else host_r.ctypes.data,
             C.c_void_p(self.workspace.data_ptr()), pb.value, C.c_void_p(scratch.data_ptr()), sb.value, C.byref(h))
@@ -131,6 +165,16 @@ class DeviceProblem:
         self.handle = h
         self.n, self.m = p.n, p.m
         self.kind = q.kind
+        self.persistent_bytes = int(pb.value)
+        self.part = part
+        if part is None:
+            self.rank, self.nranks = 0, 1
+            self.rows = (0, p.n, 0, p.m)
+            self.plans = None
+        else:
+            self.rank, self.nranks = part.rank, part.me.nranks
+            self.rows = (part.me.n0, part.me.n1, part.me.m0, part.me.m1)
+            self.plans = part.plans
         info = nat.ProblemInfo()
         nat.check(lib.aqp_problem_get_info(h, C.byref(info)))
         self.info = info
@@ -148,17 +192,6 @@ class DeviceProblem:
                                                  C.c_void_p(scratch.data_ptr()), scratch.numel() * 8),
                   "aqp_problem_scale")
         return D[: self.n], E[: self.m]
-
-    def shard(self, rank: int, nranks: int, n0: int, n1: int, m0: int, m1: int):
-        """Restrict this rank's passes to rows [n0,n1) of A'/Q and [m0,m1) of A
-        (aqp_problem_shard)."""
-        sh = nat.Shard(rank=rank, nranks=nranks, n0=n0, n1=n1, m0=m0, m1=m1)
-        nat.check(self.ctx.lib.aqp_problem_shard(self.handle, C.byref(sh)), "aqp_problem_shard")
-        info = nat.ProblemInfo()
-        nat.check(self.ctx.lib.aqp_problem_get_info(self.handle, C.byref(info)))
-        self.info = info
-        self.rank, self.nranks = rank, nranks
-        self.rows = (n0, n1, m0, m1)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -236,7 +269,9 @@ class DeviceSolver:
         nat.check(self.lib.aqp_solver_reset_window(self.handle))
 
     def read(self, which: int) -> np.ndarray:
-        length = self.prob.m if which in (self.Y, self.YRAY0, self.YRAY1) else self.prob.n
+        """The whole vector, or (row shard) this rank's slice of it."""
+        n0, n1, m0, m1 = self.prob.rows
+        length = m1 - m0 if which in (self.Y, self.YRAY0, self.YRAY1) else n1 - n0
         out = np.empty(length, dtype=np.float64)
         nat.check(self.lib.aqp_solver_read(self.handle, int(which), out.ctypes.data, length), "aqp_solver_read")
         return out

@@ -202,14 +202,16 @@ class _Run:
         self.params = params
         self.progress = progress
         ctx = DeviceContext.get(device)
-        self.dev = DeviceProblem(problem, ctx)
+        self.group = group
         self.scaling = getattr(params, "scaling", None)
         if self.scaling is not None and group is not None:
             raise ValueError("scaling is not available for row-sharded solves")
-        if group is not None:  # row shard of a multi-GPU solve (shard.py)
-            from .shard import rows_of
+        if group is not None:  # row shard of a multi-GPU solve: this rank's rows only (shard.py)
+            from .shard import local_part, plan
 
-            self.dev.shard(group.rank, group.nranks, *rows_of(problem, group))
+            self.dev = DeviceProblem(problem, ctx, part=local_part(problem, plan(problem, group.nranks), group.rank))
+        else:
+            self.dev = DeviceProblem(problem, ctx)
         gamma = params.gamma_sys if params.gamma_sys is not None else certify.default_gamma_sys(problem)
         self.gamma_sys = gamma
         self.con_scale = certify.finite_bound_scale(problem.con_bounds)
@@ -234,11 +236,15 @@ class _Run:
                 tol_scale=ip.scale, tol_floor=ip.floor, diag_bound=problem.quad.diag_bound(),
                 adaptive=ip.adaptive, max_inner=ip.max_inner, halpern=params.halpern)
         if group is not None:
-            self.solver.problem_host = problem  # for the gather halos (shard.halos)
             group.connect(self.solver)
 
+    def read(self, which: int) -> np.ndarray:
+        """A whole vector; a row shard joins the ranks' slices (collective)."""
+        out = self.checker.read(which)
+        return out if self.group is None else self.group.concat(out)
+
     def report(self, cr, need_slack: bool) -> ResidualReport:
-        slack = self.checker.read(DeviceSolver.DUAL_SLACK) if need_slack else None
+        slack = self.read(DeviceSolver.DUAL_SLACK) if need_slack else None
         return certify.report_from_check(cr, self.con_scale, self.cost_inf, slack)
 
     # certification on the original problem (identity unless scaling is on)
@@ -316,10 +322,10 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
     n_outer = n_inner = restarts = 0
 
     def finish(status, report, cert):
-        x = run.checker.read(DeviceSolver.X_EVAL)
-        y = run.checker.read(DeviceSolver.Y)
+        x = run.read(DeviceSolver.X_EVAL)
+        y = run.read(DeviceSolver.Y)
         if report.dual_slack is None:
-            report = dataclasses.replace(report, dual_slack=run.checker.read(DeviceSolver.DUAL_SLACK))
+            report = dataclasses.replace(report, dual_slack=run.read(DeviceSolver.DUAL_SLACK))
         return SolveResult(status=status, x=x, y=y, report=report, certificate=cert,
                            outer_iterations=n_outer, inner_iterations=n_inner, restarts=restarts,
                            seconds=time.monotonic() - start)
@@ -411,13 +417,13 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
         for j in order:
             hit = certify.primal_ray_test(cr, j, params.eps_inf)
             if hit is not None:
-                ray = run.checker.read(DeviceSolver.YRAY0 + j)
+                ray = run.read(DeviceSolver.YRAY0 + j)
                 return finish(SolveStatus.PRIMAL_INFEASIBLE, report,
                               Certificate(CertificateKind.PRIMAL_RAY, ray, hit[0], hit[1]))
         for j in order:
             hit = certify.dual_ray_test(cr, j, params.eps_tol, params.eps_inf, run.gamma_sys)
             if hit is not None:
-                ray = run.checker.read(DeviceSolver.XRAY0 + j)
+                ray = run.read(DeviceSolver.XRAY0 + j)
                 return finish(SolveStatus.DUAL_INFEASIBLE, report,
                               Certificate(CertificateKind.DUAL_RAY, ray, hit[0], hit[1]))
         run.mark_cert()

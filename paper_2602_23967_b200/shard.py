@@ -29,6 +29,7 @@ Two peer groups drive the same kernels:
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import threading
 from typing import List, Optional, Sequence, Tuple
 
@@ -84,48 +85,186 @@ def partition(problem, nranks: int) -> List[Rows]:
     return [(cx[k], cx[k + 1], cy[k], cy[k + 1]) for k in range(nranks)]
 
 
-def halos(problem, parts: Sequence[Rows]):
-    """Gather halos per rank: rank k gathers x only at the columns of its rows
-    of A and of the full symmetric Q, and y only at the columns of its rows of
-    A' (= the rows of A having a nonzero in its columns).  Returns two lists of
-    [lo, hi) ranges (global indices; empty ranges as (0, 0))."""
+@dataclasses.dataclass(frozen=True)
+class RankPlan:
+    """What rank `rank` stores and gathers (aqp_shard_desc).
+
+    * rows [n0, n1) of A' and of the full symmetric Q, rows [m0, m1) of A;
+    * the uploaded A block = rows ``ywin`` of A (the rank's own rows plus every
+      row with a nonzero in columns [n0, n1), i.e. the sources of its A'
+      rows), from which the device keeps rows [m0, m1) and builds A' rows
+      [n0, n1);
+    * the uploaded P block = upper-triangle rows [q_row0, n1) (its own rows
+      plus every row j < n0 with an upper entry in columns [n0, n1), the
+      sources of the mirrored lower part);
+    * gather halos ``xhalo`` (columns of its rows of A and Q) and ``yhalo``
+      (columns of its rows of A'), and the windows ``xwin`` / ``ywin`` =
+      halo hull its own rows: the only entries of x / y it ever holds.
+    """
+
+    rank: int
+    nranks: int
+    n0: int
+    n1: int
+    m0: int
+    m1: int
+    q_row0: int
+    xhalo: Tuple[int, int]
+    yhalo: Tuple[int, int]
+    xwin: Tuple[int, int]
+    ywin: Tuple[int, int]
+    a_local_nnz: int
+    at_local_nnz: int
+    q_local_nnz: int
+
+
+def _row_extents(indptr: np.ndarray, indices: np.ndarray, ncols: int):
+    """First / last column of every CSR row (sorted rows); empty rows: (ncols, -1)."""
+    indptr = np.asarray(indptr)
+    nz = np.diff(indptr) > 0
+    lo = np.full(len(indptr) - 1, ncols, dtype=np.int64)
+    hi = np.full(len(indptr) - 1, -1, dtype=np.int64)
+    idx = np.asarray(indices)
+    lo[nz] = idx[indptr[:-1][nz]]
+    hi[nz] = idx[indptr[1:][nz] - 1]
+    return lo, hi
+
+
+def _hull(*ranges) -> Tuple[int, int]:
+    rs = [(int(a), int(b)) for a, b in ranges if b > a]
+    if not rs:
+        return (0, 0)
+    return (min(a for a, _ in rs), max(b for _, b in rs))
+
+
+def plan(problem, nranks: int, parts: Optional[Sequence[Rows]] = None) -> List[RankPlan]:
+    """Row partition plus, per rank, the blocks it uploads, its gather halos
+    and windows.  O(n + m) plus two bincounts over the nonzeros; every rank
+    computes the identical plan from the same problem."""
+    parts = list(parts) if parts is not None else partition(problem, nranks)
     a = problem.constraint_matrix
     n, m = problem.n, problem.m
     ip, ix = np.asarray(a.indptr), np.asarray(a.indices)
-    arow = np.repeat(np.arange(m), np.diff(ip))
+    alo, ahi = _row_extents(ip, ix, n)
+    colcnt = np.bincount(ix, minlength=n) if a.nnz else np.zeros(n, dtype=np.int64)
+    ccum = np.concatenate([[0], np.cumsum(colcnt)])
     q = problem.quad
-    if q.kind == "sparse":
-        up = q.upper
+    pq = q if q.kind == "sparse" else (q.p if q.kind == "sparse_low_rank" else None)
+    if pq is not None:
+        up = pq.upper
         qp, qi = np.asarray(up.indptr), np.asarray(up.indices)
-        qrow = np.repeat(np.arange(n), np.diff(qp))
-    xr, yr = [], []
-    for n0, n1, m0, m1 in parts:
-        lo, hi = n, 0
-        cols = ix[ip[m0]:ip[m1]]                      # A rows [m0, m1)
-        if cols.size:
-            lo, hi = min(lo, int(cols.min())), max(hi, int(cols.max()) + 1)
-        if q.kind == "sparse":
-            ucols = qi[qp[n0]:qp[n1]]                  # upper rows [n0, n1): j >= i
-            if ucols.size:
-                lo, hi = min(lo, int(ucols.min())), max(hi, int(ucols.max()) + 1)
-            sel = (qi >= n0) & (qi < n1)               # mirrored lower part: rows j < i
-            if sel.any():
-                r = qrow[sel]
-                lo, hi = min(lo, int(r.min())), max(hi, int(r.max()) + 1)
-        xr.append((lo, hi) if hi > lo else (0, 0))
-        sel = (ix >= n0) & (ix < n1)                   # A' rows [n0, n1) = A's columns
-        if sel.any():
-            r = arow[sel]
-            yr.append((int(r.min()), int(r.max()) + 1))
-        else:
-            yr.append((0, 0))
-    return xr, yr
+        qlo, qhi = _row_extents(qp, qi, n)
+        rows = np.repeat(np.arange(n), np.diff(qp))
+        offd = qi != rows
+        # full row i of Q = upper row i + mirrored off-diagonal upper entries (j, i)
+        fullcnt = np.diff(qp) + np.bincount(qi[offd], minlength=n)
+        fcum = np.concatenate([[0], np.cumsum(fullcnt)])
+    out = []
+    for r, (n0, n1, m0, m1) in enumerate(parts):
+        xr = [(int(alo[m0:m1].min(initial=n)), int(ahi[m0:m1].max(initial=-1)) + 1)]
+        q_row0 = n0
+        qloc = 0
+        if pq is not None:
+            xr.append((n0, int(qhi[n0:n1].max(initial=-1)) + 1))  # upper part: j >= i
+            src = np.flatnonzero((qhi[:n0] >= n0) & (qlo[:n0] < n1))  # mirrored part: rows j < n0
+            if src.size:
+                q_row0 = int(src[0])
+                xr.append((q_row0, n0))
+            qloc = int(fcum[n1] - fcum[n0])
+        xhalo = _hull(*xr)
+        yrows = np.flatnonzero((alo < n1) & (ahi >= n0))  # rows of A with a nonzero in columns [n0, n1)
+        yhalo = (int(yrows[0]), int(yrows[-1]) + 1) if yrows.size else (0, 0)
+        out.append(RankPlan(rank=r, nranks=nranks, n0=n0, n1=n1, m0=m0, m1=m1, q_row0=q_row0,
+                            xhalo=xhalo, yhalo=yhalo, xwin=_hull(xhalo, (n0, n1)), ywin=_hull(yhalo, (m0, m1)),
+                            a_local_nnz=int(ip[m1] - ip[m0]), at_local_nnz=int(ccum[n1] - ccum[n0]),
+                            q_local_nnz=qloc))
+    return out
 
 
-def _set_halos(solver, problem, nranks):
-    parts = partition(problem, nranks)
-    xr, yr = halos(problem, parts)
-    solver.set_halos(xr, yr)
+@dataclasses.dataclass
+class LocalPart:
+    """Host views of one rank's blocks (inputs of aqp_problem_create with a
+    shard descriptor) plus the plan of every rank."""
+
+    plans: List[RankPlan]
+    rank: int
+    a_indptr: np.ndarray
+    a_indices: np.ndarray
+    a_data: np.ndarray
+    q_indptr: Optional[np.ndarray]
+    q_indices: Optional[np.ndarray]
+    q_data: Optional[np.ndarray]
+    q_vec: Optional[np.ndarray]       # DiagonalQuad values or P's diagonal, entries [n0, n1)
+    r_indptr: Optional[np.ndarray]
+    r_indices: Optional[np.ndarray]
+    r_data: Optional[np.ndarray]
+    r_dense: bool
+    cost: np.ndarray
+    var_lo: np.ndarray
+    var_hi: np.ndarray
+    con_lo: np.ndarray
+    con_hi: np.ndarray
+
+    @property
+    def me(self) -> RankPlan:
+        return self.plans[self.rank]
+
+
+def _block(indptr, indices, data, r0, r1):
+    indptr = np.asarray(indptr)
+    k0, k1 = int(indptr[r0]), int(indptr[r1])
+    return indptr[r0:r1 + 1] - k0, np.asarray(indices)[k0:k1], np.asarray(data)[k0:k1]
+
+
+def local_part(problem, plans: List[RankPlan], rank: int) -> LocalPart:
+    """This rank's blocks as host views (no copies of the big arrays)."""
+    me = plans[rank]
+    n0, n1, m0, m1 = me.n0, me.n1, me.m0, me.m1
+    a = problem.constraint_matrix
+    ai, ax, ad = _block(a.indptr, a.indices, a.data, me.ywin[0], me.ywin[1])
+    q = problem.quad
+    qi = qx = qd = qv = None
+    ri = rx = rd = None
+    dense = False
+    if q.kind == "diagonal":
+        qv = np.asarray(q.values)[n0:n1]
+    else:
+        pq = q if q.kind == "sparse" else q.p
+        qi, qx, qd = _block(pq.upper.indptr, pq.upper.indices, pq.upper.data, me.q_row0, n1)
+        qv = np.asarray(pq.diag)[n0:n1]
+        if q.kind == "sparse_low_rank":
+            from .device import _full_rows
+
+            r = q.r
+            nl = n1 - n0
+            if _full_rows(r):  # dense factor: columns [n0, n1) of every row, row-major
+                dense = True
+                rd = np.ascontiguousarray(np.asarray(r.data).reshape(r.rows, r.cols)[:, n0:n1]).reshape(-1)
+                ri = np.arange(r.rows + 1, dtype=np.int64) * nl
+                rx = None
+            else:
+                rp, rc, rv = np.asarray(r.indptr), np.asarray(r.indices), np.asarray(r.data)
+                keep = (rc >= n0) & (rc < n1)
+                rows = np.repeat(np.arange(r.rows), np.diff(rp))
+                ri = np.concatenate([[0], np.cumsum(np.bincount(rows[keep], minlength=r.rows))]).astype(np.int64)
+                rx, rd = rc[keep], rv[keep]
+    return LocalPart(plans=plans, rank=rank, a_indptr=ai, a_indices=ax, a_data=ad, q_indptr=qi, q_indices=qx,
+                     q_data=qd, q_vec=qv, r_indptr=ri, r_indices=rx, r_data=rd, r_dense=dense,
+                     cost=np.asarray(problem.cost)[n0:n1], var_lo=np.asarray(problem.var_bounds.lower)[n0:n1],
+                     var_hi=np.asarray(problem.var_bounds.upper)[n0:n1],
+                     con_lo=np.asarray(problem.con_bounds.lower)[m0:m1],
+                     con_hi=np.asarray(problem.con_bounds.upper)[m0:m1])
+
+
+def halos(problem, parts: Sequence[Rows]):
+    """Gather halos per rank (see RankPlan): two lists of [lo, hi) ranges."""
+    pl = plan(problem, len(parts), parts)
+    return [p.xhalo for p in pl], [p.yhalo for p in pl]
+
+
+def _set_halos(solver):
+    plans = solver.prob.plans
+    solver.set_halos([p.xhalo for p in plans], [p.yhalo for p in plans])
 
 
 _Handle = C.c_char * 64  # cudaIpcMemHandle_t
@@ -142,6 +281,14 @@ class PeerGroup:
 
     def agree_any(self, flag: bool) -> bool:  # pragma: no cover - interface
         raise NotImplementedError
+
+    def gather(self, arr: np.ndarray) -> List[np.ndarray]:  # pragma: no cover - interface
+        """Every rank's `arr`, in rank order (host arrays; collective)."""
+        raise NotImplementedError
+
+    def concat(self, arr: np.ndarray) -> np.ndarray:
+        """The ranks' row slices joined into the whole vector (collective)."""
+        return np.concatenate(self.gather(np.ascontiguousarray(arr)))
 
     def close(self) -> None:
         pass
@@ -182,8 +329,7 @@ class DistGroup(PeerGroup):
             self._mapped.append((int(ptr.value), o))
             bases.append(int(ptr.value))
         self.dist.barrier(group=self.group)  # every rank's mailbox is zero before anyone writes
-        if getattr(solver, "problem_host", None) is not None:
-            _set_halos(solver, solver.problem_host, self.nranks)
+        _set_halos(solver)
         solver.connect(bases)
         self.dist.barrier(group=self.group)
 
@@ -195,6 +341,11 @@ class DistGroup(PeerGroup):
             t = t.cuda()
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return bool(int(t.item()))
+
+    def gather(self, arr: np.ndarray) -> List[np.ndarray]:
+        out = [None] * self.nranks
+        self.dist.all_gather_object(out, arr, group=self.group)
+        return out
 
     def close(self) -> None:
         lib = nat.load()
@@ -209,6 +360,7 @@ class _LocalShared:
         self.barrier = threading.Barrier(nranks)
         self.bases: List[Optional[int]] = [None] * nranks
         self.flags = [False] * nranks
+        self.items: List = [None] * nranks
 
 
 class LocalGroup(PeerGroup):
@@ -228,8 +380,7 @@ class LocalGroup(PeerGroup):
         base, _ = solver.exchange_region()
         self.shared.bases[self.rank] = base
         self.shared.barrier.wait()  # all created (mailboxes zeroed) and published
-        if getattr(solver, "problem_host", None) is not None:
-            _set_halos(solver, solver.problem_host, self.nranks)
+        _set_halos(solver)
         solver.connect(list(self.shared.bases))
         # graph instantiation may synchronise the device: no rank may start
         # exchanging (spinning) while another rank still builds its graph
@@ -240,6 +391,14 @@ class LocalGroup(PeerGroup):
         sh.flags[self.rank] = bool(flag)
         sh.barrier.wait()
         out = any(sh.flags)
+        sh.barrier.wait()
+        return out
+
+    def gather(self, arr: np.ndarray) -> List[np.ndarray]:
+        sh = self.shared
+        sh.items[self.rank] = arr
+        sh.barrier.wait()
+        out = list(sh.items)
         sh.barrier.wait()
         return out
 
@@ -263,8 +422,10 @@ def solve_local(problem, params=None, nranks: int = 2, device: int = 0, timeout:
 
     def work(r):
         try:
+            from .batch import pooled_stream
+
             torch.cuda.set_device(device)
-            with torch.cuda.stream(torch.cuda.Stream(device)):
+            with torch.cuda.stream(pooled_stream(device, 1000 + r)):  # one cached stream per virtual rank
                 results[r] = solve(problem, params, device=device, group=groups[r], **kw)
         except BaseException as exc:  # reported after join
             errors[r] = exc
@@ -304,4 +465,5 @@ def rows_of(problem, group: PeerGroup) -> Rows:
     return partition(problem, group.nranks)[group.rank]
 
 
-__all__ = ["partition", "halos", "PeerGroup", "DistGroup", "LocalGroup", "solve_local", "rows_of"]
+__all__ = ["partition", "plan", "local_part", "halos", "RankPlan", "LocalPart", "PeerGroup", "DistGroup",
+           "LocalGroup", "solve_local", "rows_of"]

@@ -82,7 +82,50 @@ def test_sharded_matches_single_gpu_trajectory(cuda):
         np.testing.assert_allclose(sh.y, one.y, rtol=1e-9, atol=1e-11)
 
 
-def test_shard_rejects_low_rank(cuda):
-    p = instances.build("rqp:300:150:low_rank:0.05:3")
-    with pytest.raises(Exception, match="low-rank"):
-        shard.solve_local(p, SolverParams(), nranks=2, timeout=120)
+@pytest.mark.parametrize("spec,fname,nranks", [
+    ("rqp:300:150:low_rank:0.05:3", "ref_rqp_300_150_low_rank_0.05_3.json", 2),  # CSR R: R x all-reduced
+    ("c3:2e3:100:0", "ref_c3_2e3_100_0.json", 2),                               # dense factor R (C3 twin)
+    ("c3:2e4:100:0", "ref_c3_2e4_100_0.json", 3),
+])
+def test_sharded_low_rank_matches_reference_golden(cuda, spec, fname, nranks):
+    """Low-rank Q = P + R'R row-sharded: R is split by columns, each rank's
+    R x is a partial sum all-reduced (k values, rank order) before R'(R x)."""
+    g = golden(fname)
+    res = run_sharded(instances.build(spec), SolverParams(eps_tol=g["eps_tol"]), nranks)
+    check_golden(res, g)
+
+
+def test_sharded_sparse_c5_twin(cuda):
+    """The sparse-Q C5 twin (banded A, Q band i +- 1000) over 4 ranks."""
+    g = golden("ref_c5_5e4_500_0.json")
+    res = run_sharded(instances.build("c5:5e4:500:0"), SolverParams(eps_tol=g["eps_tol"]), 4)
+    check_golden(res, g)
+
+
+@pytest.mark.parametrize("spec", ["c5:5e4:500:0", "c5:5e4:500:0:diag", "c3:2e4:100:0"])
+def test_storage_shrinks_with_ranks(cuda, spec):
+    """Storage shards: a rank's persistent problem memory and solver workspace
+    are ~1/P of the whole problem's (instances too large
+    for one GPU)."""
+    from paper_2602_23967_b200.device import DeviceContext, DeviceProblem, DeviceSolver
+
+    p = instances.build(spec)
+    ctx = DeviceContext.get(0)
+
+    def solver_bytes(dev):
+        import ctypes as C
+
+        sz = C.c_size_t()
+        ctx.lib.aqp_solver_sizes(dev.handle, C.byref(sz))
+        return sz.value
+
+    whole = DeviceProblem(p, ctx)
+    w_prob, w_sol = whole.persistent_bytes, solver_bytes(whole)
+    whole.close()
+    P = 4
+    plans = shard.plan(p, P)
+    for r in range(P):
+        dev = DeviceProblem(p, ctx, part=shard.local_part(p, plans, r))
+        assert dev.persistent_bytes <= 1.2 * w_prob / P + (1 << 20), (r, dev.persistent_bytes, w_prob)
+        assert solver_bytes(dev) <= 1.3 * w_sol / P + (8 << 20), (r, solver_bytes(dev), w_sol)
+        dev.close()

@@ -77,7 +77,8 @@ def _dist_worker(rank, world, port, q):
         agreed = [g.agree_any(rank == 1 and k == 0) for k in range(2)]
         p = instances.build("c1:1")
         rows = shard.rows_of(p, g)
-        q.put((rank, agreed, rows))
+        joined = g.concat(np.arange(3) + 10 * rank)
+        q.put((rank, agreed, rows, joined.tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -99,8 +100,9 @@ def test_dist_group_gloo_world2():
     for pr in procs:
         pr.join(60)
         assert pr.exitcode == 0
-    (r0, a0, rows0), (r1, a1, rows1) = res
+    (r0, a0, rows0, j0), (r1, a1, rows1, j1) = res
     assert a0 == a1 == [True, False]
+    assert j0 == j1 == [0, 1, 2, 10, 11, 12]
     p = instances.build("c1:1")
     assert [rows0, rows1] == shard.partition(p, 2)
 
@@ -134,3 +136,78 @@ def test_banded_halos_are_strips():
     xr, yr = shard.halos(p, parts)
     for (n0, n1, m0, m1), (xl, xh) in zip(parts, xr):
         assert n0 - xl <= 1000 and xh - n1 <= 1000  # Q band (i +- 1000) dominates A's +- 500
+
+
+def _full_q(p):
+    q = p.quad
+    pq = q if q.kind == "sparse" else (q.p if q.kind == "sparse_low_rank" else None)
+    if pq is None:
+        return None
+    u = pq.upper.to_scipy()
+    import scipy.sparse as sp
+
+    return (u + sp.triu(u, 1).T).tocsr()
+
+
+@pytest.mark.parametrize("spec", ["c5:5e3:50:0", "c1:0", "rqp:500:300:diagonal:0.02:5", "c2:1e4:5e3:0",
+                                  "rqp:300:150:low_rank:0.05:3", "c3:2e3:100:0"])
+@pytest.mark.parametrize("nranks", [2, 3, 8])
+def test_local_parts_hold_exactly_the_rank_rows(spec, nranks):
+    """Storage shards: each rank's uploaded blocks reproduce its rows of A, A'
+    and the full symmetric Q exactly (what the device builds from them), the
+    local-nnz counts the device checks are right, and the windows cover every
+    gathered column plus the rank's own rows."""
+    p = instances.build(spec)
+    plans = shard.plan(p, nranks)
+    a = p.constraint_matrix.to_scipy().tocsr()
+    at = a.T.tocsr()
+    qf = _full_q(p)
+    for r, me in enumerate(plans):
+        part = shard.local_part(p, plans, r)
+        blk_rows = me.ywin[1] - me.ywin[0]
+        import scipy.sparse as sp
+
+        blk = sp.csr_matrix((part.a_data, part.a_indices, part.a_indptr), shape=(blk_rows, p.n))
+        # A rows [m0, m1) and A' rows [n0, n1) from the block
+        assert (blk[me.m0 - me.ywin[0]:me.m1 - me.ywin[0]] != a[me.m0:me.m1]).nnz == 0
+        assert me.a_local_nnz == a[me.m0:me.m1].nnz
+        bt = blk.T.tocsr()[me.n0:me.n1]
+        want = at[me.n0:me.n1]
+        assert bt.nnz == want.nnz == me.at_local_nnz
+        # the block's rows are global rows ywin[0] + local
+        assert np.array_equal(np.sort(bt.indices + me.ywin[0]), np.sort(want.indices))
+        c = [a[me.m0:me.m1].indices]
+        if qf is not None:
+            ub = sp.csr_matrix((part.q_data, part.q_indices, part.q_indptr), shape=(me.n1 - me.q_row0, p.n))
+            full = sp.vstack([sp.csr_matrix((me.q_row0, p.n)), ub, sp.csr_matrix((p.n - me.n1, p.n))]).tocsr()
+            rows = (full + sp.triu(full, 1).T).tocsr()[me.n0:me.n1]
+            assert (rows != qf[me.n0:me.n1]).nnz == 0
+            assert me.q_local_nnz == qf[me.n0:me.n1].nnz
+            c.append(qf[me.n0:me.n1].indices)
+        cols = np.concatenate(c)
+        assert cols.size == 0 or (cols.min() >= me.xhalo[0] and cols.max() < me.xhalo[1])
+        assert me.xwin[0] <= min(me.xhalo[0], me.n0) and me.xwin[1] >= max(me.xhalo[1], me.n1)
+        ys = at[me.n0:me.n1].indices
+        assert ys.size == 0 or (ys.min() >= me.yhalo[0] and ys.max() < me.yhalo[1])
+        assert me.ywin[0] <= me.m0 and me.ywin[1] >= me.m1
+        assert np.array_equal(part.cost, p.cost[me.n0:me.n1])
+        assert np.array_equal(part.con_lo, p.con_bounds.lower[me.m0:me.m1])
+        if p.quad.kind == "sparse_low_rank":  # columns [n0, n1) of R
+            rr = p.quad.r.to_scipy().tocsc()[:, me.n0:me.n1].tocsr()
+            if part.r_dense:
+                assert np.array_equal(part.r_data.reshape(p.quad.r.rows, -1), rr.toarray())
+            else:
+                got = sp.csr_matrix((part.r_data, part.r_indices - me.n0, part.r_indptr), shape=rr.shape)
+                assert (got != rr).nnz == 0
+
+
+def test_banded_storage_shrinks_with_ranks():
+    """C5-type (banded) windows are the rank's rows plus boundary strips, so a
+    rank's stored rows and gather windows shrink ~1/P."""
+    p = instances.build("c5:5e4:500:0")
+    for P in (2, 4, 8):
+        for me in shard.plan(p, P):
+            assert (me.xwin[1] - me.xwin[0]) <= p.n / P + 2 * 1000 + 2
+            assert (me.ywin[1] - me.ywin[0]) <= p.m / P + 2 * 600
+            assert me.a_local_nnz + me.at_local_nnz + me.q_local_nnz <= 1.1 * (
+                2 * p.constraint_matrix.nnz + 2 * p.quad.upper.nnz) / P
