@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define AQP_ABI_VERSION 2
+#define AQP_ABI_VERSION 3
 
 enum {
   AQP_OK = 0,
@@ -188,6 +188,15 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *desc,
                        void *persistent, size_t persistent_bytes,
                        void *scratch, size_t scratch_bytes, aqp_problem **out);
 int aqp_problem_get_info(const aqp_problem *p, aqp_problem_info *out);
+/* Optional coalesced SELL-32 copies of the uniform short-row matrices (A,
+ * A', Q, R, R' whose every row fits one thread and whose 32-row slices pad
+ * <= 1/8): the SpMV passes then load a warp's k-th nonzeros contiguously
+ * (C5: A x 2.57 -> 2.07 ms, Q x 1.25 -> 1.17 ms).  The layout is planned in
+ * aqp_problem_create; the caller supplies device memory of
+ * aqp_problem_sell_bytes (0: nothing to attach) and attaches it before
+ * creating solvers.  The buffer must outlive the problem. */
+int aqp_problem_sell_bytes(const aqp_problem *p, size_t *bytes);
+int aqp_problem_attach_sell(aqp_problem *p, void *buf, size_t bytes);
 
 /* Device-side Ruiz (ruiz_iters rounds of inf-norm equilibration of
  * K = [[Q, A'], [A, 0]]) and optional Pock-Chambolle (alpha = 1, l1) scaling,
@@ -198,6 +207,36 @@ int aqp_problem_get_info(const aqp_problem *p, aqp_problem_info *out);
 int aqp_problem_scale(aqp_problem *p, int ruiz_iters, int pock_chambolle, double *D, double *E, void *scratch,
                       size_t scratch_bytes);
 int aqp_problem_destroy(aqp_problem *p);
+
+/* Validation flags and setup scalars of a created problem, computed on the
+ * device (replaces the host passes of anchorqp's solve entry):
+ *   model.py:168-206   validate(): the host raises the FIRST violation in the
+ *                      reference's order (var bounds, con bounds, cost, A, Q)
+ *   certify.py:54-60   finite_bound_scale(con_bounds) -> con_scale; |c|_inf
+ *   linalg.py:218-220  SparseQuad.inf_norm_bound (bitwise: sequential row /
+ *                      column sums in numpy.bincount's order) -> q_bound
+ *                      (DIAGONAL: max(values))
+ *   linalg.py:260-263  low rank: r_one = max col abs sum of R, r_inf = max row
+ *                      abs sum (r_inf_done = 0 for a row shard: R's rows span
+ *                      every rank's columns, the host computes it)
+ *   linalg.py:167-168,215-216,252-258  diag_bound
+ * Indices are global; a row shard reports its own rows / columns (maxima,
+ * flags and first indices combine across ranks by max / or / min). */
+typedef struct {
+  int32_t var_nan, var_wrong_inf, con_nan, con_wrong_inf;
+  int64_t var_first_inverted, con_first_inverted;  /* -1: none */
+  int32_t cost_nonfinite, a_nonfinite, q_nonfinite, r_inf_done;
+  double con_scale, cost_inf, q_bound, r_one, r_inf, diag_bound;
+} aqp_setup_info;
+int aqp_problem_setup_info(aqp_problem *p, aqp_setup_info *out);
+
+/* Bulk synchronous copies between host memory (pageable, e.g. numpy) and
+ * device memory of ctx's device, staged through a process-wide pool of
+ * pinned buffers by 8 host threads (~45 GB/s H2D on the B200 box vs ~10 GB/s
+ * pageable).  aqp_d2h first synchronises ctx's stream (the source is
+ * produced there). */
+int aqp_h2d(aqp_ctx *ctx, void *dev_dst, const void *host_src, size_t bytes);
+int aqp_d2h(aqp_ctx *ctx, void *host_dst, const void *dev_src, size_t bytes);
 
 
 

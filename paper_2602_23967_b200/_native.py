@@ -22,7 +22,7 @@ c_double_p = C.POINTER(C.c_double)
 c_int64_p = C.POINTER(C.c_int64)
 
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class ShardDesc(C.Structure):
@@ -58,6 +58,17 @@ class ProblemInfo(C.Structure):
         ("a_items", C.c_int64), ("at_items", C.c_int64), ("q_items", C.c_int64),
         ("quad_kind", C.c_int32), ("r_dense", C.c_int32),
         ("persistent_bytes", C.c_size_t),
+    ]
+
+
+class SetupInfo(C.Structure):
+    _fields_ = [
+        ("var_nan", C.c_int32), ("var_wrong_inf", C.c_int32), ("con_nan", C.c_int32), ("con_wrong_inf", C.c_int32),
+        ("var_first_inverted", C.c_int64), ("con_first_inverted", C.c_int64),
+        ("cost_nonfinite", C.c_int32), ("a_nonfinite", C.c_int32), ("q_nonfinite", C.c_int32),
+        ("r_inf_done", C.c_int32),
+        ("con_scale", C.c_double), ("cost_inf", C.c_double), ("q_bound", C.c_double), ("r_one", C.c_double),
+        ("r_inf", C.c_double), ("diag_bound", C.c_double),
     ]
 
 
@@ -118,6 +129,11 @@ SIGNATURES = {
                                      C.POINTER(_P)]),
     "aqp_problem_get_info": (C.c_int, [_P, C.POINTER(ProblemInfo)]),
     "aqp_problem_destroy": (C.c_int, [_P]),
+    "aqp_problem_setup_info": (C.c_int, [_P, C.POINTER(SetupInfo)]),
+    "aqp_problem_sell_bytes": (C.c_int, [_P, C.POINTER(C.c_size_t)]),
+    "aqp_problem_attach_sell": (C.c_int, [_P, _P, C.c_size_t]),
+    "aqp_h2d": (C.c_int, [_P, _P, _P, C.c_size_t]),
+    "aqp_d2h": (C.c_int, [_P, _P, _P, C.c_size_t]),
     "aqp_solver_sizes": (C.c_int, [_P, C.POINTER(C.c_size_t)]),
     "aqp_solver_create": (C.c_int, [_P, C.POINTER(SolverParamsC), _P, C.c_size_t, C.POINTER(_P)]),
     "aqp_solver_destroy": (C.c_int, [_P]),

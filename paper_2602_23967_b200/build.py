@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libaqp.so")
 OBJDIR = os.path.join(ROOT, "build", "obj")
-SOURCES = ["aqp_problem.cu", "aqp_solver.cu", "aqp_registry.cu", "aqp_scale.cu"]
+SOURCES = ["aqp_problem.cu", "aqp_solver.cu", "aqp_registry.cu", "aqp_scale.cu", "aqp_xfer.cu", "aqp_setup.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

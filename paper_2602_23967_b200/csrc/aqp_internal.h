@@ -28,6 +28,7 @@ struct CsrStore {
   double *seg_part = nullptr;
   unsigned *seg_ticket = nullptr;
   int64_t seg_cap = 0;
+  int64_t *sell_off = nullptr;  // SELL-32 slice offsets (rows / 32 + 2), planned by plan_sell
 };
 
 void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz);
@@ -39,6 +40,8 @@ int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool 
 int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool strict, Bump &scratch,
                    int64_t *nfull_out, int64_t row_base = 0, int64_t r0 = 0, int64_t r1 = -1);
 size_t transpose_scratch_bytes(int64_t nnz, int64_t cols);
+// synchronous staged host <-> device copy (aqp_xfer.cu)
+int bulk_copy(int device, void *dev, void *host, size_t bytes, bool h2d);
 size_t symmetrize_scratch_bytes(int64_t nnz, int64_t n);
 }  // namespace aqp
 
@@ -65,6 +68,7 @@ struct aqp_problem {
   aqp::CsrStore sA, sAt, sQ, sR, sRt;
   aqp::DevCsr A, At, Q, R, Rt;
   int64_t q_full_nnz = 0;
+  int64_t sell_total[5] = {};  // padded SELL-32 entries of A, A', Q, R, R' (0: no SELL copy)
   int r_dense = 0;  // R held dense row-major in R.val (R.rows x n); no R' CSR
   double *qdiag = nullptr;  // Q's diagonal when split out of its CSR (DevCsr::diag)
   double *c = nullptr, *vlo = nullptr, *vhi = nullptr, *qd = nullptr, *clo = nullptr, *chi = nullptr;

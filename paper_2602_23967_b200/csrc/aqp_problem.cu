@@ -14,7 +14,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -23,6 +25,26 @@
 #include "aqp_internal.h"
 
 namespace aqp {
+
+// AQP_TIMING=1: stream-synchronised wall time of each setup step of
+// aqp_problem_create, printed to stderr (diagnostics only; off by default)
+static void step_mark(cudaStream_t st, const char *what) {
+  static const bool on = [] {
+    const char *e = getenv("AQP_TIMING");
+    return e && e[0] == '1';
+  }();
+  static auto t = std::chrono::steady_clock::now();
+  if (!on) return;
+  cudaStreamSynchronize(st);
+  const auto now = std::chrono::steady_clock::now();
+  if (what) fprintf(stderr, "AQP_TIMING %s %.4f\n", what, std::chrono::duration<double>(now - t).count());
+  t = now;
+}
+struct StepTimer {
+  cudaStream_t st;
+  explicit StepTimer(cudaStream_t s) : st(s) { step_mark(st, nullptr); }
+  void operator()(const char *what) { step_mark(st, what); }
+};
 
 static thread_local std::string g_last_error;
 void set_error(const std::string &msg) { g_last_error = msg; }
@@ -279,51 +301,50 @@ __global__ void k_fill_sell(const int *__restrict__ ptr, const int *__restrict__
   }
 }
 
-// stream-ordered (cudaMallocAsync / cudaFreeAsync): no device-wide
-// synchronisation while other streams (concurrent solves) are working
+// The SELL-32 arrays live in a caller-provided buffer (aqp_problem_attach_sell),
+// the offsets in the problem's persistent workspace: dropping them frees nothing.
 void free_sell(DevCsr &M, cudaStream_t st) {
-  if (M.sell_off) cudaFreeAsync(const_cast<int64_t *>(M.sell_off), st);
-  if (M.sell_idx) cudaFreeAsync(const_cast<int *>(M.sell_idx), st);
-  if (M.sell_val) cudaFreeAsync(const_cast<double *>(M.sell_val), st);
+  (void)st;
   M.sell_off = nullptr;
   M.sell_idx = nullptr;
   M.sell_val = nullptr;
 }
 
-template <class P>
-static int build_sell(aqp_ctx *ctx, DevCsr &M, const P *hp) {
-  free_sell(M, ctx->stream);
+// 32 * (longest row of each 32-row slice); w[nsl] = 0 so the exclusive scan
+// ends with the total
+__global__ void k_sell_width(const int *__restrict__ ptr, int rows, int64_t nsl, int64_t *__restrict__ w) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > nsl) return;
+  int mx = 0;
+  for (int64_t r = 32 * s; r < 32 * s + 32 && r < rows; ++r) mx = max(mx, ptr[r + 1] - ptr[r]);
+  w[s] = 32 * (int64_t)mx;
+}
+
+// SELL-32 layout of a uniform, non-strict matrix: slice offsets into `off`
+// (rows/32 + 2 entries of persistent storage); *total = padded entries, or 0
+// when the padding exceeds 1/8 (measured on C2: SELL speeds the A pass, 8
+// nonzeros every row: 38.7 -> 33.8 us, but slows the padded A' and Q passes,
+// ~2x padding: 33.0 -> 39.6 and 49.0 -> 51.1 us; on C5 A x 2.57 -> 2.07 ms,
+// Q x 1.25 -> 1.17 ms).
+static int plan_sell(aqp_ctx *ctx, const DevCsr &M, int64_t *off, Bump &scratch, int64_t *total) {
+  *total = 0;
   const char *e = getenv("AQP_SELL");
-  if (e && e[0] == '0') return AQP_OK;
-  const int64_t nsl = ((int64_t)M.rows + 31) / 32;
-  std::vector<int64_t> off((size_t)nsl + 1);
-  int64_t total = 0;
-  for (int64_t s = 0; s < nsl; ++s) {
-    int64_t w = 0;
-    for (int64_t r = 32 * s; r < std::min<int64_t>(32 * s + 32, M.rows); ++r) w = std::max<int64_t>(w, (int64_t)(hp[r + 1] - hp[r]));
-    off[s] = total;
-    total += 32 * w;
-  }
-  off[nsl] = total;
-  const int64_t nnz = (int64_t)(hp[M.rows] - hp[0]);
-  // Only near-constant row lengths: measured on C2, SELL speeds the A pass
-  // (8 nonzeros every row: 38.7 -> 33.8 us) but slows the padded A' and Q
-  // passes (~2x padding: 33.0 -> 39.6 and 49.0 -> 51.1 us)
-  if (total > nnz + nnz / 8 + 32) return AQP_OK;
-  int64_t *doff = nullptr;
-  int *sidx = nullptr;
-  double *sval = nullptr;
+  if ((e && e[0] == '0') || !M.uniform || M.rows == 0 || !off) return AQP_OK;
   cudaStream_t st = ctx->stream;
-  AQP_CUDA(cudaMallocAsync(&doff, (nsl + 1) * sizeof(int64_t), st));
-  AQP_CUDA(cudaMallocAsync(&sidx, std::max<int64_t>(total, 1) * sizeof(int), st));
-  AQP_CUDA(cudaMallocAsync(&sval, std::max<int64_t>(total, 1) * sizeof(double), st));
-  AQP_CUDA(cudaMemcpyAsync(doff, off.data(), (nsl + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  k_fill_sell<<<(M.rows + 255) / 256, 256, 0, ctx->stream>>>(M.ptr, M.idx, M.val, M.rows, doff, sidx, sval);
+  const int64_t nsl = ((int64_t)M.rows + 31) / 32;
+  scratch.used = 0;
+  int64_t *w = (int64_t *)scratch.take((nsl + 1) * sizeof(int64_t));
+  size_t need = 0;
+  AQP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, w, off, (int)(nsl + 1), st));
+  void *tmp = scratch.take(need);
+  if (scratch.overflow) return AQP_OK;  // no room to plan: the CSR path serves
+  k_sell_width<<<(int)((nsl + 256) / 256), 256, 0, st>>>(M.ptr, M.rows, nsl, w);
   AQP_CUDA(cudaGetLastError());
-  M.sell_off = doff;
-  M.sell_idx = sidx;
-  M.sell_val = sval;
-  AQP_CUDA(cudaStreamSynchronize(st));  // `off` is a pageable local
+  AQP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, w, off, (int)(nsl + 1), st));
+  int64_t tot = 0;
+  AQP_CUDA(cudaMemcpyAsync(&tot, off + nsl, sizeof(tot), cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  if (tot <= M.nnz + M.nnz / 8 + 32) *total = tot;
   return AQP_OK;
 }
 
@@ -357,6 +378,31 @@ __global__ void k_split_diag(const int *__restrict__ optr, const int *__restrict
   }
 }
 
+__global__ void k_row_maxlen(const int *__restrict__ ptr, int rows, int *out) {
+  int mx = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+    mx = max(mx, ptr[r + 1] - ptr[r]);
+  atomicMax(out, mx);
+}
+
+// the uniform plan: THREAD items over rows [256 b, 256 b + 256)
+__global__ void k_uniform_plan(const int *__restrict__ ptr, int rows, int nitems, PlanItem *plan) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nitems) return;
+  PlanItem it{};
+  it.row0 = b * kThreads;
+  it.row1 = min(rows, (b + 1) * kThreads);
+  it.k0 = ptr[it.row0];
+  it.k1 = ptr[it.row1];
+  it.kind = kItemThread;
+  plan[b] = it;
+}
+
+// Plan the SpMV work of M (rows from M.ptr on the device, or from the given
+// host copy).  Without a host copy, a uniform matrix (every row <= the
+// THREAD length, no staging, not strict -- the common case, every C2 / C5
+// pass but A') is planned on the device; otherwise the row pointers come to
+// the host for plan_rows.
 int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *host_ptr64, bool strict,
                 PlanItem *plan_dev, int64_t plan_cap, double *seg_part, unsigned *seg_ticket,
                 int64_t seg_cap, bool may_stage) {
@@ -368,11 +414,47 @@ int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *h
   double staged_min = may_stage ? 8.0 : 1e300;
   if (const char *e = getenv("AQP_STAGED_MIN"))  // A/B knob for the matrices that may stage (A')
     if (may_stage) staged_min = atof(e);
+  cudaStream_t st = ctx->stream;
+  free_sell(M, st);  // a re-plan drops the SELL copy (aqp_problem_attach_sell rebuilds it)
+  std::vector<int> dev_ptr_copy;
+  if (!host_ptr32 && !host_ptr64) {
+    const bool staged = !strict && M.rows > 0 && (double)M.nnz >= staged_min * (double)M.rows;
+    if (!strict && !staged && M.rows > 0) {
+      int *dmax = (int *)seg_ticket;  // seg_ticket is zeroed scratch until the plan is in place
+      int mx = 0;
+      AQP_CUDA(cudaMemsetAsync(dmax, 0, sizeof(int), st));
+      k_row_maxlen<<<std::min(148 * 16, (M.rows + 255) / 256), 256, 0, st>>>(M.ptr, M.rows, dmax);
+      AQP_CUDA(cudaGetLastError());
+      AQP_CUDA(cudaMemcpyAsync(&mx, dmax, sizeof(int), cudaMemcpyDeviceToHost, st));
+      AQP_CUDA(cudaMemsetAsync(dmax, 0, sizeof(int), st));
+      AQP_CUDA(cudaStreamSynchronize(st));
+      if (mx <= kThreadRowMax) {
+        const int nitems = (M.rows + kThreads - 1) / kThreads;
+        if (nitems > plan_cap) return fail(AQP_ENOMEM, "plan capacity exceeded");
+        k_uniform_plan<<<(nitems + 255) / 256, 256, 0, st>>>(M.ptr, M.rows, nitems, plan_dev);
+        AQP_CUDA(cudaGetLastError());
+        M.plan = plan_dev;
+        M.nitems = nitems;
+        M.smem_bytes = 0;
+        M.uniform = 1;
+        M.nlongseg = 0;
+        M.seg_part = seg_part;
+        M.seg_ticket = seg_ticket;
+        step_mark(st, "  finish_plan.device_uniform");
+        return AQP_OK;
+      }
+    }
+    dev_ptr_copy.resize((size_t)M.rows + 1);
+    AQP_CUDA(cudaMemcpyAsync(dev_ptr_copy.data(), M.ptr, (M.rows + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+    AQP_CUDA(cudaStreamSynchronize(st));
+    host_ptr32 = dev_ptr_copy.data();
+  }
   const int64_t nnz_rows = M.rows > 0 ? (host_ptr64 ? host_ptr64[M.rows] - host_ptr64[0]
                                                     : (int64_t)host_ptr32[M.rows] - host_ptr32[0]) : 0;
   const bool staged = !strict && M.rows > 0 && (double)nnz_rows >= staged_min * (double)M.rows;
   std::vector<PlanItem> items = host_ptr64 ? plan_rows(host_ptr64, M.rows, strict, &nlong, staged)
                                            : plan_rows(host_ptr32, M.rows, strict, &nlong, staged);
+  step_mark(ctx->stream, "  finish_plan.plan_rows");
   if ((int64_t)items.size() > plan_cap) return fail(AQP_ENOMEM, "plan capacity exceeded");
   if (nlong > seg_cap) return fail(AQP_ENOMEM, "segment capacity exceeded");
   AQP_CUDA(cudaMemcpyAsync(plan_dev, items.data(), items.size() * sizeof(PlanItem), cudaMemcpyHostToDevice,
@@ -392,8 +474,6 @@ int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *h
   M.nlongseg = nlong;
   M.seg_part = seg_part;
   M.seg_ticket = seg_ticket;
-  if (M.uniform && !strict) return host_ptr64 ? build_sell(ctx, M, host_ptr64) : build_sell(ctx, M, host_ptr32);
-  free_sell(M, ctx->stream);
   return AQP_OK;
 }
 
@@ -408,6 +488,7 @@ void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz) {
   s.seg_cap = nnz / kSegNnz + nnz / kTileNnz + 2;  // each long row adds at most one partial segment
   s.seg_part = (double *)b.take(2 * s.seg_cap * sizeof(double));
   s.seg_ticket = (unsigned *)b.take(s.seg_cap * sizeof(unsigned));
+  s.sell_off = (int64_t *)b.take((rows / 32 + 2) * sizeof(int64_t));
 }
 
 // Upload an int64 CSR (device pointers) into int32 storage and plan it.
@@ -419,13 +500,15 @@ int upload_csr(aqp_ctx *ctx, CsrStore &s, DevCsr &M, int64_t rows, int64_t cols,
   AQP_TRY(to_i32(d_idx, s.idx, nnz, cols - 1, d_bad, st));
   if (nnz) AQP_CUDA(cudaMemcpyAsync(s.val, d_val, nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
   AQP_CUDA(cudaMemsetAsync(s.seg_ticket, 0, s.seg_cap * sizeof(unsigned), st));
+  step_mark(st, "  upload_csr.convert");
   M.rows = (int)rows;
   M.cols = (int)cols;
   M.nnz = nnz;
   M.ptr = s.ptr;
   M.idx = s.idx;
   M.val = s.val;
-  return finish_plan(ctx, M, nullptr, host_ptr, strict, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap,
+  // non-strict plans start on the device (uniform matrices never visit the host)
+  return finish_plan(ctx, M, nullptr, strict ? host_ptr : nullptr, strict, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap,
                      false);
 }
 
@@ -489,10 +572,7 @@ int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool 
   T.ptr = t.ptr;
   T.idx = t.idx;
   T.val = t.val;
-  std::vector<int> hptr(rows_t + 1);
-  AQP_CUDA(cudaMemcpyAsync(hptr.data(), t.ptr, (rows_t + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
-  AQP_CUDA(cudaStreamSynchronize(st));
-  return finish_plan(ctx, T, hptr.data(), nullptr, strict, t.plan, t.plan_cap, t.seg_part, t.seg_ticket, t.seg_cap,
+  return finish_plan(ctx, T, nullptr, nullptr, strict, t.plan, t.plan_cap, t.seg_part, t.seg_ticket, t.seg_cap,
                      true);
 }
 
@@ -529,7 +609,9 @@ int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool s
     int end_bit = 1;
     while ((1LL << end_bit) <= (int64_t)n) ++end_bit;
     size_t need = tb;
+    step_mark(st, "  symmetrize.keys");
     AQP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, keys, keys2, vals, vals2, (int)n2, 0, end_bit, st));
+    step_mark(st, "  symmetrize.sort");
     int ndiag = 0;
     AQP_CUDA(cudaMemcpyAsync(&ndiag, counts + n, sizeof(int), cudaMemcpyDeviceToHost, st));
     AQP_CUDA(cudaStreamSynchronize(st));
@@ -550,10 +632,8 @@ int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool s
   F.idx = f.idx;
   F.val = f.val;
   *nfull_out = nfull;
-  std::vector<int> hptr(n + 1);
-  AQP_CUDA(cudaMemcpyAsync(hptr.data(), f.ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
-  AQP_CUDA(cudaStreamSynchronize(st));
-  return finish_plan(ctx, F, hptr.data(), nullptr, strict, f.plan, f.plan_cap, f.seg_part, f.seg_ticket, f.seg_cap,
+  step_mark(st, "  symmetrize.gather_scan");
+  return finish_plan(ctx, F, nullptr, nullptr, strict, f.plan, f.plan_cap, f.seg_part, f.seg_ticket, f.seg_cap,
                      false);
 }
 
@@ -649,12 +729,10 @@ static int split_q_diag(aqp_ctx *ctx, aqp_problem *p, Bump &scratch) {
   AQP_CUDA(cudaMemcpyAsync(optr, M.ptr, (int64_t)(n + 1) * 4, cudaMemcpyDeviceToDevice, st));
   k_split_diag<<<(n + 256) / 256, 256, 0, st>>>(optr, oidx, oval, n, M.row_off, s.ptr, s.idx, s.val, p->qdiag);
   AQP_CUDA(cudaGetLastError());
-  std::vector<int> hptr((size_t)n + 1);
-  AQP_CUDA(cudaMemcpyAsync(hptr.data(), s.ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
-  AQP_CUDA(cudaStreamSynchronize(st));
   M.nnz = nnz - n;
   M.diag = p->qdiag;
-  AQP_TRY(finish_plan(ctx, M, hptr.data(), nullptr, false, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap,
+  M.ptr = s.ptr;
+  AQP_TRY(finish_plan(ctx, M, nullptr, nullptr, false, s.plan, s.plan_cap, s.seg_part, s.seg_ticket, s.seg_cap,
                       false));
   if (!M.uniform) return fail(AQP_ECUDA, "diagonal split changed the Q plan kind");
   return AQP_OK;
@@ -884,11 +962,14 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
     return code;
   };
   AQP_CUDA(cudaMemsetAsync(p->bad, 0, 64, st));
+  StepTimer tm(st);
   if (!sh) {
     rc = upload_csr(ctx, p->sA, p->A, d->m, d->n, d->a_indptr, d->a_indices, d->a_data, d->a_nnz, host_a_indptr,
                     false, p->bad);
     if (rc) return cleanup(rc);
+    tm("A_convert_plan");
     rc = transpose_csr(ctx, p->A, p->sAt, p->At, false, sc);
+    tm("At_transpose_plan");
   } else {
     rc = shard_a(ctx, p, d, host_a_indptr, scratch, scratch_bytes);
   }
@@ -925,11 +1006,14 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
     Bump rest;
     rest.base = static_cast<char *>(scratch) + ((ub.used + 255) & ~size_t(255));
     rest.cap = scratch_bytes - ((ub.used + 255) & ~size_t(255));
+    tm("Q_convert");
     rc = symmetrize_csr(ctx, U, p->sQ, p->Q, false, rest, &p->q_full_nnz, urow0, p->n0, p->n1);
     if (rc) return cleanup(rc);
+    tm("Q_symmetrize_plan");
     if (sh && p->q_full_nnz != sh->q_local_nnz) return cleanup(fail(AQP_EINVAL, "q_local_nnz does not match the P block"));
     rc = split_q_diag(ctx, p, rest);
     if (rc) return cleanup(rc);
+    tm("Q_split_diag_plan");
     if (n) AQP_CUDA(cudaMemcpyAsync(p->qd, d->q_diag, n * 8, cudaMemcpyDeviceToDevice, st));
     if (d->quad_kind == AQP_QUAD_SPARSE_LOW_RANK && d->r_dense) {
       // full rows: the CSR values are R row-major (a shard: its columns
@@ -963,9 +1047,20 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
   rc = build_cones(ctx, p->vlo, p->vhi, n, p->cone_r, p->recc_x, 0);
   if (!rc) rc = build_cones(ctx, p->clo, p->chi, m, p->cone_y, p->recc_s, 1);
   if (rc) return cleanup(rc);
+  {  // SELL-32 layouts of the uniform matrices (filled by aqp_problem_attach_sell)
+    CsrStore *stores[5] = {&p->sA, &p->sAt, &p->sQ, &p->sR, &p->sRt};
+    DevCsr *mats[5] = {&p->A, &p->At, &p->Q, &p->R, &p->Rt};
+    for (int i = 0; i < 5; ++i) {
+      if (i == 2 && d->quad_kind == AQP_QUAD_DIAGONAL) continue;
+      if (i >= 3 && (d->quad_kind != AQP_QUAD_SPARSE_LOW_RANK || p->r_dense)) continue;
+      rc = plan_sell(ctx, *mats[i], stores[i]->sell_off, sc, &p->sell_total[i]);
+      if (rc) return cleanup(rc);
+    }
+  }
   int bad = 0;
   AQP_CUDA(cudaMemcpyAsync(&bad, p->bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   AQP_CUDA(cudaStreamSynchronize(st));
+  tm("vectors_cones_sell_plan");
   if (bad) return cleanup(fail(AQP_EINVAL, "index out of range in CSR upload"));
   std::memset(&p->info, 0, sizeof(p->info));
   p->info.a_nnz = p->A.nnz;
@@ -979,6 +1074,46 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
   p->info.q_items = p->Q.nitems;
   p->info.persistent_bytes = b.used;
   *out = p;
+  return AQP_OK;
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+int aqp_problem_sell_bytes(const aqp_problem *p, size_t *bytes) {
+  if (!p || !bytes) return fail(AQP_EINVAL, "NULL argument");
+  size_t b = 0;
+  for (int i = 0; i < 5; ++i)
+    if (p->sell_total[i]) b += align256((size_t)p->sell_total[i] * 4) + align256((size_t)p->sell_total[i] * 8);
+  *bytes = b;
+  return AQP_OK;
+}
+
+int aqp_problem_attach_sell(aqp_problem *p, void *buf, size_t bytes) {
+  if (!p) return fail(AQP_EINVAL, "NULL argument");
+  size_t need = 0;
+  AQP_TRY(aqp_problem_sell_bytes(p, &need));
+  if (need == 0) return AQP_OK;
+  if (!buf || bytes < need) return fail(AQP_ENOMEM, "SELL buffer too small (aqp_problem_sell_bytes)");
+  AQP_CUDA(cudaSetDevice(p->ctx->device));
+  cudaStream_t st = p->ctx->stream;
+  CsrStore *stores[5] = {&p->sA, &p->sAt, &p->sQ, &p->sR, &p->sRt};
+  DevCsr *mats[5] = {&p->A, &p->At, &p->Q, &p->R, &p->Rt};
+  char *at = static_cast<char *>(buf);
+  for (int i = 0; i < 5; ++i) {
+    const int64_t tot = p->sell_total[i];
+    if (!tot) continue;
+    DevCsr &M = *mats[i];
+    int *sidx = reinterpret_cast<int *>(at);
+    at += align256((size_t)tot * 4);
+    double *sval = reinterpret_cast<double *>(at);
+    at += align256((size_t)tot * 8);
+    k_fill_sell<<<(M.rows + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, M.val, M.rows, stores[i]->sell_off, sidx, sval);
+    AQP_CUDA(cudaGetLastError());
+    M.sell_off = stores[i]->sell_off;
+    M.sell_idx = sidx;
+    M.sell_val = sval;
+  }
+  AQP_CUDA(cudaStreamSynchronize(st));
   return AQP_OK;
 }
 

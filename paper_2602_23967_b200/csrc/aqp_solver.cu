@@ -2176,7 +2176,11 @@ int aqp_solver_read(aqp_solver *s, int which, double *host_out, int64_t len) {
     src = which == 1 ? pick3(v.ys, s->h.ycur) : pick3(v.xs, s->h.xcur);
   }
   cudaStream_t st = s->p->ctx->stream;
-  for (int64_t off = 0; off < need; off += (int64_t)aqp_solver::kBounce) {  // via the pinned bounce buffer
+  if (need > (int64_t)aqp_solver::kBounce) {  // bulk: the multi-threaded pinned pipeline (aqp_xfer.cu)
+    AQP_CUDA(cudaStreamSynchronize(st));
+    AQP_TRY(bulk_copy(s->p->ctx->device, const_cast<double *>(src), host_out, (size_t)need * 8, false));
+  }
+  for (int64_t off = 0; off < need && need <= (int64_t)aqp_solver::kBounce; off += (int64_t)aqp_solver::kBounce) {
     const int64_t len = std::min<int64_t>(need - off, (int64_t)aqp_solver::kBounce);
     AQP_CUDA(cudaMemcpyAsync(s->bounce, src + off, len * 8, cudaMemcpyDeviceToHost, st));
     AQP_CUDA(cudaStreamSynchronize(st));
@@ -2211,7 +2215,11 @@ int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, do
   // gather window (the whole vector unsharded)
   const int64_t w0 = p->xwin[2 * p->rank], w1 = p->xwin[2 * p->rank + 1];
   double *win = pick3(v.xbb, 0) - v.xoff + w0;
-  for (int64_t off = 0; off < w1 - w0; off += (int64_t)aqp_solver::kBounce) {
+  if (w1 - w0 > (int64_t)aqp_solver::kBounce) {  // bulk: the multi-threaded pinned pipeline (aqp_xfer.cu)
+    AQP_CUDA(cudaStreamSynchronize(st));
+    AQP_TRY(bulk_copy(p->ctx->device, win, const_cast<double *>(host_v0 + w0), (size_t)(w1 - w0) * 8, true));
+  }
+  for (int64_t off = 0; off < w1 - w0 && w1 - w0 <= (int64_t)aqp_solver::kBounce; off += (int64_t)aqp_solver::kBounce) {
     const int64_t len = std::min<int64_t>(w1 - w0 - off, (int64_t)aqp_solver::kBounce);
     AQP_CUDA(cudaStreamSynchronize(st));  // the bounce buffer is free again
     std::memcpy(s->bounce, host_v0 + w0 + off, len * 8);

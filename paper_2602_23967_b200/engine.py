@@ -15,6 +15,9 @@ from __future__ import annotations
 import dataclasses
 import enum
 import math
+import os
+import sys
+import threading
 import time
 from typing import Callable, Optional, Sequence
 
@@ -24,7 +27,7 @@ from . import _native as nat
 from . import certify
 from .certify import Certificate, CertificateKind, ResidualReport
 from .device import DeviceContext, DeviceProblem, DeviceSolver
-from .model import QpProblem, validate
+from .model import QpProblem, raise_first_violation, validate_dims
 
 # engine.py:26-49
 OMEGA_MIN = 1e-6
@@ -36,6 +39,30 @@ THETA_BACKOFF_FLOOR = 1e-2
 STALL_CHECKS = 8
 STALL_IMPROVEMENT = 0.99
 PROBE_INNER_TOL = 1e-12  # applied on the device (OpGrad<true>::finalize)
+
+
+class _Phases:
+    """AQP_PHASES=1: device-synchronised wall time per setup / loop phase of a
+    solve, printed to stderr (diagnostics of the end-to-end path only)."""
+
+    def __init__(self):
+        self.on = os.environ.get("AQP_PHASES", "") == "1"
+        self.t = time.perf_counter()
+        self.acc = {}
+
+    def __call__(self, name):
+        if not self.on:
+            return
+        import torch
+
+        torch.cuda.synchronize()
+        now = time.perf_counter()
+        self.acc[name] = self.acc.get(name, 0.0) + now - self.t
+        self.t = now
+
+    def dump(self):
+        if self.on:
+            print("AQP_PHASES " + " ".join(f"{k}={v:.4f}" for k, v in self.acc.items()), file=sys.stderr, flush=True)
 
 
 class SolveStatus(str, enum.Enum):
@@ -180,24 +207,74 @@ def pid_update(rs: _Round, dx: float, dy: float, params: SolverParams) -> float:
     return min(max(math.exp(log_omega), OMEGA_MIN), OMEGA_MAX)
 
 
-def estimate_eta(solver: DeviceSolver, problem: QpProblem, params: SolverParams) -> float:
+class _StartVector:
+    """The power iteration's first start vector, drawn exactly as the
+    reference draws it (``default_rng(norm_seed).standard_normal(cols)``,
+    linalg.py:293-294) on a host thread while the problem uploads -- numpy
+    releases the GIL while it fills the array (0.5 s at C5).  Redraws continue
+    from the same generator."""
+
+    def __init__(self, cols: int, seed: int):
+        self.cols = cols
+        self.rng = np.random.default_rng(seed)
+        self.v = None
+        self.thread = threading.Thread(target=self._draw, daemon=True)
+        self.thread.start()
+
+    def _draw(self):
+        self.v = self.rng.standard_normal(self.cols)
+
+    def first(self) -> np.ndarray:
+        self.thread.join()
+        return self.v
+
+
+def estimate_eta(solver: DeviceSolver, problem: QpProblem, params: SolverParams,
+                 start: Optional[_StartVector] = None) -> float:
     """initialize()'s step scale (engine.py:178-183, linalg.py:287-312)."""
     a = problem.constraint_matrix
     if a.nnz == 0:
         return ETA_UNCONSTRAINED
-    rng = np.random.default_rng(params.norm_seed)
-    for _ in range(8):
-        v = rng.standard_normal(a.cols)  # start vector drawn exactly as the reference draws it
+    start = start or _StartVector(a.cols, params.norm_seed)
+    for attempt in range(8):
+        v = start.first() if attempt == 0 else start.rng.standard_normal(a.cols)
         est, annihilated = solver.estimate_norm(v, params.norm_iters)
         if not annihilated:
             return params.eta_scale / est
     return ETA_UNCONSTRAINED
 
 
+def _setup_info(dev: DeviceProblem, problem: QpProblem, group):
+    """Device validation flags + setup scalars; a row shard combines every
+    rank's (flags: or, first inverted index: min, maxima: max) and computes
+    R's row sums, which span every rank's columns, on the host."""
+    info = dev.setup_info()
+    if group is None:
+        return info
+    ints = ("var_nan", "var_wrong_inf", "con_nan", "con_wrong_inf", "cost_nonfinite", "a_nonfinite", "q_nonfinite")
+    maxes = ("con_scale", "cost_inf", "q_bound", "r_one", "diag_bound")
+    mine = np.array([getattr(info, f) for f in ints + maxes] + [info.var_first_inverted, info.con_first_inverted],
+                    dtype=np.float64)
+    rows = np.stack(group.gather(mine))
+    for i, f in enumerate(ints):
+        setattr(info, f, int(rows[:, i].max()))
+    for i, f in enumerate(maxes):
+        setattr(info, f, float(rows[:, len(ints) + i].max()))
+    for i, f in enumerate(("var_first_inverted", "con_first_inverted")):
+        col = rows[:, len(ints) + len(maxes) + i]
+        col = col[col >= 0]
+        setattr(info, f, int(col.min()) if col.size else -1)
+    if problem.quad.kind == "sparse_low_rank" and not info.r_inf_done:
+        info.r_inf = float(problem.quad.r.row_abs_sums().max(initial=0.0))  # linalg.py:262
+        info.r_inf_done = 1
+    return info
+
+
 class _Run:
     """One solve: device objects + the reference's loop locals."""
 
-    def __init__(self, problem: QpProblem, params: SolverParams, progress, device: int, group=None):
+    def __init__(self, problem: QpProblem, params: SolverParams, progress, device: int, group=None, ph=None):
+        ph = ph or _Phases()
         self.problem = problem
         self.params = params
         self.progress = progress
@@ -212,12 +289,23 @@ class _Run:
             self.dev = DeviceProblem(problem, ctx, part=local_part(problem, plan(problem, group.nranks), group.rank))
         else:
             self.dev = DeviceProblem(problem, ctx)
-        gamma = params.gamma_sys if params.gamma_sys is not None else certify.default_gamma_sys(problem)
+        if ph.on:
+            ph.acc["problem_create"] = self.dev.timing.get("create", 0.0)
+            ph.t += self.dev.timing.get("create", 0.0)
+            ph("problem_upload")
+        # validate()'s data checks and the setup scalars, on the device
+        info = _setup_info(self.dev, problem, group)
+        raise_first_violation(problem, info)
+        q_bound = info.q_bound  # QuadOperator.inf_norm_bound (linalg.py:218-220, 260-263)
+        if problem.quad.kind == "sparse_low_rank":
+            q_bound = q_bound + info.r_one * info.r_inf
+        gamma = params.gamma_sys if params.gamma_sys is not None else 1.0 + q_bound  # certify.py:167-169
         self.gamma_sys = gamma
-        self.con_scale = certify.finite_bound_scale(problem.con_bounds)
-        self.cost_inf = certify.linf(problem.cost)
+        self.con_scale = info.con_scale  # certify.py:54-60
+        self.cost_inf = info.cost_inf
+        ph("setup_scalars")
         ip = params.inner
-        diag_bound = problem.quad.diag_bound()
+        diag_bound = info.diag_bound
         self.checker_dev = None
         if self.scaling is not None:
             # iterate on an equilibrated copy; certify on the original (checker)
@@ -233,10 +321,11 @@ class _Run:
         if self.checker_dev is not None:
             self.checker = DeviceSolver(
                 self.checker_dev, eps_tol=params.eps_tol, eps_inf=params.eps_inf, gamma_sys=gamma,
-                tol_scale=ip.scale, tol_floor=ip.floor, diag_bound=problem.quad.diag_bound(),
+                tol_scale=ip.scale, tol_floor=ip.floor, diag_bound=info.diag_bound,
                 adaptive=ip.adaptive, max_inner=ip.max_inner, halpern=params.halpern)
         if group is not None:
             group.connect(self.solver)
+        ph("solver_create")
 
     def read(self, which: int) -> np.ndarray:
         """A whole vector; a row shard joins the ranks' slices (collective)."""
@@ -307,13 +396,17 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
     with the group's other ranks; every rank calls solve
     with the same problem and params and gets the same result."""
     params = params or SolverParams()
+    ph = _Phases()
     problem = QpProblem.from_any(problem)
-    validate(problem)
+    validate_dims(problem)  # the data checks of validate() run on the device (_Run)
+    ph("validate")
     start = time.monotonic()
-    run = _Run(problem, params, progress, device, group)
+    v0 = _StartVector(problem.n, params.norm_seed) if problem.constraint_matrix.nnz else None
+    run = _Run(problem, params, progress, device, group, ph)
     sol = run.solver
     rs = _Round(omega=params.omega0, eta=0.0, theta=params.theta)
-    rs.eta = estimate_eta(sol, problem, params)
+    rs.eta = estimate_eta(sol, problem, params, v0)
+    ph("estimate_eta")
     tol0 = params.inner.initial if params.inner.adaptive else params.inner.fixed_tol
     sc = nat.Scalars()
     sc.eta, sc.omega, sc.theta, sc.inner_tol = rs.eta, rs.omega, rs.theta, tol0
@@ -322,18 +415,23 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
     n_outer = n_inner = restarts = 0
 
     def finish(status, report, cert):
+        ph("loop")
         x = run.read(DeviceSolver.X_EVAL)
         y = run.read(DeviceSolver.Y)
         if report.dual_slack is None:
             report = dataclasses.replace(report, dual_slack=run.read(DeviceSolver.DUAL_SLACK))
+        ph("read_back")
+        ph.dump()
         return SolveResult(status=status, x=x, y=y, report=report, certificate=cert,
                            outer_iterations=n_outer, inner_iterations=n_inner, restarts=restarts,
                            seconds=time.monotonic() - start)
 
     # sharded: reading the slack is collective, so every rank reads it
     want_slack = progress is not None or group is not None
+    ph("init")
     cr = run.check(with_rays=False)
     report = run.report(cr, want_slack)
+    ph("first_check")
     rs.best_residual_round_start = report.kkt_max
     rs.last_check_kkt = report.kkt_max
     if progress is not None:

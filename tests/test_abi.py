@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_ctypes_binding_covers_header(lib):
     assert sorted(nat.SIGNATURES) == declared()
-    assert lib.aqp_abi_version() == nat.ABI_VERSION == 2
+    assert lib.aqp_abi_version() == nat.ABI_VERSION == 3
 
 
 def test_library_is_sm100a():
@@ -51,10 +51,12 @@ def _c_layout():
 #include <stddef.h>
 #include "aqp.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(aqp_problem_desc), sizeof(aqp_problem_info), sizeof(aqp_solver_params),
-         sizeof(aqp_scalars), sizeof(aqp_check_result), sizeof(aqp_shard_desc));
-  printf("%zu %zu %zu %zu %zu\n", offsetof(aqp_problem_desc, con_hi), offsetof(aqp_check_result, xr_qd_inf),
-         offsetof(aqp_scalars, have_avg_prev), offsetof(aqp_problem_desc, shard), offsetof(aqp_shard_desc, yw));
+  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(aqp_problem_desc), sizeof(aqp_problem_info),
+         sizeof(aqp_solver_params), sizeof(aqp_scalars), sizeof(aqp_check_result), sizeof(aqp_shard_desc),
+         sizeof(aqp_setup_info));
+  printf("%zu %zu %zu %zu %zu %zu\n", offsetof(aqp_problem_desc, con_hi), offsetof(aqp_check_result, xr_qd_inf),
+         offsetof(aqp_scalars, have_avg_prev), offsetof(aqp_problem_desc, shard), offsetof(aqp_shard_desc, yw),
+         offsetof(aqp_setup_info, diag_bound));
   return 0;
 }'''
     exe = os.path.join(ROOT, "build", "abi_probe")
@@ -67,9 +69,10 @@ int main(void) {
 def test_struct_layouts_match_c():
     sizes, offs = _c_layout()
     assert sizes == [ctypes.sizeof(nat.ProblemDesc), ctypes.sizeof(nat.ProblemInfo), ctypes.sizeof(nat.SolverParamsC),
-                     ctypes.sizeof(nat.Scalars), ctypes.sizeof(nat.CheckResult), ctypes.sizeof(nat.ShardDesc)]
+                     ctypes.sizeof(nat.Scalars), ctypes.sizeof(nat.CheckResult), ctypes.sizeof(nat.ShardDesc),
+                     ctypes.sizeof(nat.SetupInfo)]
     assert offs == [nat.ProblemDesc.con_hi.offset, nat.CheckResult.xr_qd_inf.offset, nat.Scalars.have_avg_prev.offset,
-                    nat.ProblemDesc.shard.offset, nat.ShardDesc.yw.offset]
+                    nat.ProblemDesc.shard.offset, nat.ShardDesc.yw.offset, nat.SetupInfo.diag_bound.offset]
 
 
 def test_product_fails_loudly_without_device(monkeypatch):
