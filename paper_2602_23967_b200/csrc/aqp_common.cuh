@@ -419,6 +419,16 @@ struct DevCsr {
   const int64_t *sell_off = nullptr;
   const int *sell_idx = nullptr;
   const double *sell_val = nullptr;
+  // SELL-P (block-sorted SELL, for the A' of banded problems): within every
+  // 256-row block the rows are ordered by length (descending, stable), and
+  // the SELL-32 slices run over those sorted POSITIONS -- position p holds
+  // row (p & ~255) + sell_perm[p] -- so a slice's rows have near-equal
+  // lengths (1.12x padding on C5's A' instead of 1.72x).  Rows longer than
+  // kThreadRowMax are not in the slices (the block sums them together).  Row
+  // sums stay sequential per row; the epilogue runs in natural row order after
+  // a shared-memory hand-off.  (Sorting within a warp only -- no block
+  // barrier, natural slice widths -- measured slower: C5 A' 2.80 ms.)
+  const uint8_t *sell_perm = nullptr;
   // full symmetric Q of a uniform plan: its diagonal moved out of the CSR into
   // diag[local row].  A row's upper sum starts with diag * x[row] -- the
   // diagonal is the first j >= i entry, so the order is unchanged -- and the

@@ -28,7 +28,8 @@ struct CsrStore {
   double *seg_part = nullptr;
   unsigned *seg_ticket = nullptr;
   int64_t seg_cap = 0;
-  int64_t *sell_off = nullptr;  // SELL-32 slice offsets (rows / 32 + 2), planned by plan_sell
+  int64_t *sell_off = nullptr;  // SELL-32 slice offsets (8 per 256-row block + 2), planned by plan_sell
+  uint8_t *sell_perm = nullptr;  // SELL-P position -> row within its 256-row block (rows bytes)
 };
 
 void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz);
@@ -42,6 +43,7 @@ int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool s
 size_t transpose_scratch_bytes(int64_t nnz, int64_t cols);
 // synchronous staged host <-> device copy (aqp_xfer.cu)
 int bulk_copy(int device, void *dev, void *host, size_t bytes, bool h2d);
+int xfer_init(int device);
 size_t symmetrize_scratch_bytes(int64_t nnz, int64_t n);
 }  // namespace aqp
 
@@ -69,11 +71,13 @@ struct aqp_problem {
   aqp::DevCsr A, At, Q, R, Rt;
   int64_t q_full_nnz = 0;
   int64_t sell_total[5] = {};  // padded SELL-32 entries of A, A', Q, R, R' (0: no SELL copy)
+  bool sell_sorted[5] = {};    // ... in the SELL-P (block-sorted) layout
   int r_dense = 0;  // R held dense row-major in R.val (R.rows x n); no R' CSR
   double *qdiag = nullptr;  // Q's diagonal when split out of its CSR (DevCsr::diag)
   double *c = nullptr, *vlo = nullptr, *vhi = nullptr, *qd = nullptr, *clo = nullptr, *chi = nullptr;
   int8_t *cone_r = nullptr, *recc_x = nullptr, *cone_y = nullptr, *recc_s = nullptr;
   int *bad = nullptr;
+  void *setup_scratch = nullptr;  // 256 B of device memory for aqp_problem_setup_info
   aqp_problem_info info{};
   // row shard (aqp_shard_desc): this rank stores rows [n0,n1) of A' / Q and
   // [m0,m1) of A only; gathered vectors live in the windows xwin / ywin

@@ -381,6 +381,87 @@ __device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, c
   }
 }
 
+// One 256-row block of a SELL-P matrix (DevCsr::sell_perm): thread t sums
+// the row at sorted position t from the SELL slices (coalesced index / value
+// loads, the row's nonzeros in column order), the block sums its long rows
+// together (tree order, like the WARP / LONG items), the sums meet in shared
+// memory, and thread t runs the epilogue of row 256 b + t -- the same row ->
+// thread map (so the same reductions) as the natural uniform path.
+template <class Op>
+__device__ __forceinline__ void spmv_sellp_block(const DevCsr &M, const Op &o, RedVals<Op::NS, Op::NM> &acc,
+                                                 double *sred) {
+  __shared__ double ssum[kThreads];
+  __shared__ int lrow[kThreads];
+  __shared__ int nlr;
+  const int blk = blockIdx.x * kThreads, t = threadIdx.x;
+  const int rn = blk + t;  // epilogue row (= sorted position index)
+  using RowIn = typename RowInOf<Op>::type;
+  RowIn rin{};
+  const bool has = rn < M.rows;
+  if constexpr (RowInOf<Op>::value && !RowInLateOf<Op>::value)
+    if (has) rin = o.load_row(rn);
+  const int r = has ? blk + (int)__ldg(M.sell_perm + rn) : blk;
+  int b = 0, e = 0;
+  if (has) {
+    b = __ldg(M.ptr + r);
+    e = __ldg(M.ptr + r + 1);
+  }
+  const int len = e - b;
+  const bool lng = has && len > kThreadRowMax;
+  if (t == 0) nlr = 0;
+  if (has && !lng) {
+    const int rg = r + M.row_off;
+    double lo = 0.0, up = 0.0;
+    if (Op::SYM && M.diag) up = __ldg(M.diag + r) * o.gather(rg);
+    const int64_t base = __ldg(M.sell_off + (rn >> 5)) + (rn & 31);
+    for (int k = 0; k < len; k += AQP_GATHER_BATCH) {
+      int cc[AQP_GATHER_BATCH];
+      double pv[AQP_GATHER_BATCH];
+#pragma unroll
+      for (int u = 0; u < AQP_GATHER_BATCH; ++u) {
+        const bool in = k + u < len;
+        cc[u] = in ? __ldg(M.sell_idx + base + 32 * (k + u)) : 0;
+        pv[u] = in ? __ldg(M.sell_val + base + 32 * (k + u)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < AQP_GATHER_BATCH; ++u)
+        if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);
+#pragma unroll
+      for (int u = 0; u < AQP_GATHER_BATCH; ++u) {
+        if (k + u < len) {
+          if (Op::SYM && cc[u] < rg) lo += pv[u]; else up += pv[u];
+        }
+      }
+    }
+    ssum[r - blk] = Op::SYM ? lo + up : up;
+  }
+  if (__syncthreads_count(lng)) {  // rare: rows longer than a thread's share
+    if (lng) lrow[atomicAdd(&nlr, 1)] = r;  // any order: each long row is summed on its own
+    __syncthreads();
+    const int nl = nlr;
+    for (int i = 0; i < nl; ++i) {
+      const int rr = lrow[i], rg = rr + M.row_off;
+      RedVals<2, 0> lu;
+      lu.zero();
+      if (Op::SYM && M.diag && t == 0) lu.s[1] = __ldg(M.diag + rr) * o.gather(rg);
+      for (int k = __ldg(M.ptr + rr) + t, ke = __ldg(M.ptr + rr + 1); k < ke; k += kThreads) {
+        const int c = __ldg(M.idx + k);
+        const double pv = __ldg(M.val + k) * o.gather(c);
+        if (Op::SYM && c < rg) lu.s[0] += pv; else lu.s[1] += pv;
+      }
+      block_reduce<2, 0>(lu, sred);
+      if (t == 0) ssum[rr - blk] = Op::SYM ? lu.s[0] + lu.s[1] : lu.s[1];
+      __syncthreads();  // sred is reused by the next row
+    }
+  }
+  __syncthreads();
+  if (has) {
+    const double val = ssum[t];
+    if constexpr (RowInOf<Op>::value && RowInLateOf<Op>::value) rin = o.load_row(rn);
+    if constexpr (RowInOf<Op>::value) o.row_in(rn, val, rin, acc); else o.row(rn, val, acc);
+  }
+}
+
 template <class Op, bool UNIFORM = false>
 __global__ void __launch_bounds__(kThreads, UNIFORM ? UniformBlocksOf<Op>::value : AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
   constexpr int NS = Op::NS, NM = Op::NM;
@@ -407,6 +488,26 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? UniformBlocksOf<Op>::value
   RedVals<NS, NM> acc;
   acc.zero();
   spmv_item<Op, UNIFORM>(M, it, o, acc, sprod, scol, sred);
+  pdl_trigger();
+  if constexpr (Op::FINAL) {
+    if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred)) o.finalize(acc);
+  }
+}
+
+// a SELL-P matrix (DevCsr::sell_perm): its own instantiation, so the extra
+// registers of the sorted path never touch the natural uniform kernels
+template <class Op>
+__global__ void __launch_bounds__(kThreads, UniformBlocksOf<Op>::value) spmv_sellp_op(DevCsr M, Op op, GridRed g) {
+  constexpr int NS = Op::NS, NM = Op::NM;
+  pdl_wait();
+  trace_mark(g, 0);
+  if (op.skip()) return;
+  Op o = op;
+  o.prepare();
+  __shared__ double sred[kWarps * kMaxRed];
+  RedVals<NS, NM> acc;
+  acc.zero();
+  spmv_sellp_block<Op>(M, o, acc, sred);
   pdl_trigger();
   if constexpr (Op::FINAL) {
     if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred)) o.finalize(acc);

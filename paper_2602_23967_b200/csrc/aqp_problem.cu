@@ -308,6 +308,7 @@ void free_sell(DevCsr &M, cudaStream_t st) {
   M.sell_off = nullptr;
   M.sell_idx = nullptr;
   M.sell_val = nullptr;
+  M.sell_perm = nullptr;
 }
 
 // 32 * (longest row of each 32-row slice); w[nsl] = 0 so the exclusive scan
@@ -320,32 +321,99 @@ __global__ void k_sell_width(const int *__restrict__ ptr, int rows, int64_t nsl,
   w[s] = 32 * (int64_t)mx;
 }
 
-// SELL-32 layout of a uniform, non-strict matrix: slice offsets into `off`
-// (rows/32 + 2 entries of persistent storage); *total = padded entries, or 0
-// when the padding exceeds 1/8 (measured on C2: SELL speeds the A pass, 8
-// nonzeros every row: 38.7 -> 33.8 us, but slows the padded A' and Q passes,
-// ~2x padding: 33.0 -> 39.6 and 49.0 -> 51.1 us; on C5 A x 2.57 -> 2.07 ms,
-// Q x 1.25 -> 1.17 ms).
-static int plan_sell(aqp_ctx *ctx, const DevCsr &M, int64_t *off, Bump &scratch, int64_t *total) {
+// SELL-P: sort every 256-row block's rows by length, descending and stable
+// (long rows, > kThreadRowMax, and the padding rows of the last block get key
+// 0 and sort last); perm[p] = local row at position p; w[slice] = 32 * the
+// slice's first (= longest) key; *long_nnz += nonzeros of the long rows.
+__global__ void __launch_bounds__(256) k_sellp_sort(const int *__restrict__ ptr, int rows, uint8_t *__restrict__ perm,
+                                                    int64_t *__restrict__ w, unsigned long long *long_nnz) {
+  using Sort = cub::BlockRadixSort<int, 256, 1, int>;
+  __shared__ typename Sort::TempStorage tmp;
+  const int r = blockIdx.x * 256 + threadIdx.x;
+  const int len = r < rows ? ptr[r + 1] - ptr[r] : 0;
+  if (len > kThreadRowMax) atomicAdd(long_nnz, (unsigned long long)len);
+  int key[1] = {len <= kThreadRowMax ? len : 0};
+  int val[1] = {(int)threadIdx.x};
+  Sort(tmp).SortDescending(key, val, 0, 6);
+  const int64_t p = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (p < rows) perm[p] = (uint8_t)val[0];
+  if ((threadIdx.x & 31) == 0) w[p >> 5] = 32 * (int64_t)key[0];
+}
+
+// SELL layout of a non-strict matrix into `off` (+ `perm` for SELL-P):
+//   natural SELL-32 when the matrix is uniform and its slices pad <= 1/8
+//     (measured on C2: SELL speeds the A pass, 8 nonzeros every row: 38.7 ->
+//     33.8 us, but slows the ~2x padded A' and Q passes: 33.0 -> 39.6 and
+//     49.0 -> 51.1 us; on C5 A x 2.57 -> 2.07 ms, Q x 1.25 -> 1.17 ms);
+//   else, for a matrix that would STAGE (mean row >= 8, A' only: the C5
+//     A'), SELL-P (sorted within 256-row blocks) when that pads <= 30% and
+//     the long rows hold <= 5% of the nonzeros (C5 P1: 2.55 -> 2.38 ms; on
+//     C2's short random rows the block barrier made it slower, 34 -> 44 us);
+//   else none (*total = 0).
+static int plan_sell(aqp_ctx *ctx, const DevCsr &M, int64_t *off, uint8_t *perm, bool may_sort, Bump &scratch,
+                     int64_t *total, bool *sorted) {
   *total = 0;
+  *sorted = false;
   const char *e = getenv("AQP_SELL");
-  if ((e && e[0] == '0') || !M.uniform || M.rows == 0 || !off) return AQP_OK;
+  if ((e && e[0] == '0') || M.rows == 0 || M.nnz == 0 || !off) return AQP_OK;
   cudaStream_t st = ctx->stream;
-  const int64_t nsl = ((int64_t)M.rows + 31) / 32;
+  const int64_t nblk = ((int64_t)M.rows + 255) / 256;
+  const int64_t nw = nblk * 8;  // slice slots (the last block's beyond-rows slices have width 0)
   scratch.used = 0;
-  int64_t *w = (int64_t *)scratch.take((nsl + 1) * sizeof(int64_t));
+  int64_t *w = (int64_t *)scratch.take((nw + 1) * sizeof(int64_t));
+  unsigned long long *lnnz = (unsigned long long *)scratch.take(sizeof(unsigned long long));
   size_t need = 0;
-  AQP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, w, off, (int)(nsl + 1), st));
+  AQP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, w, off, (int)(nw + 1), st));
   void *tmp = scratch.take(need);
   if (scratch.overflow) return AQP_OK;  // no room to plan: the CSR path serves
-  k_sell_width<<<(int)((nsl + 256) / 256), 256, 0, st>>>(M.ptr, M.rows, nsl, w);
-  AQP_CUDA(cudaGetLastError());
-  AQP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, w, off, (int)(nsl + 1), st));
+  double pad = 0.125;  // AQP_SELL_PAD: A/B knob for the accepted natural padding
+  if (const char *pe = getenv("AQP_SELL_PAD")) pad = atof(pe);
+  double pad_p = 0.30;  // AQP_SELLP_PAD: the same for SELL-P (0: off)
+  if (const char *pe = getenv("AQP_SELLP_PAD")) pad_p = atof(pe);
   int64_t tot = 0;
-  AQP_CUDA(cudaMemcpyAsync(&tot, off + nsl, sizeof(tot), cudaMemcpyDeviceToHost, st));
+  if (M.uniform) {
+    AQP_CUDA(cudaMemsetAsync(w, 0, (nw + 1) * sizeof(int64_t), st));
+    k_sell_width<<<(int)((nw + 256) / 256), 256, 0, st>>>(M.ptr, M.rows, (M.rows + 31) / 32, w);
+    AQP_CUDA(cudaGetLastError());
+    AQP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, w, off, (int)(nw + 1), st));
+    AQP_CUDA(cudaMemcpyAsync(&tot, off + nw, sizeof(tot), cudaMemcpyDeviceToHost, st));
+    AQP_CUDA(cudaStreamSynchronize(st));
+    if ((double)tot <= (double)M.nnz * (1.0 + pad) + 32) {
+      *total = tot;
+      return AQP_OK;
+    }
+  }
+  if (!perm || pad_p <= 0.0 || !may_sort || (double)M.nnz < 8.0 * (double)M.rows) return AQP_OK;
+  AQP_CUDA(cudaMemsetAsync(w, 0, (nw + 1) * sizeof(int64_t), st));
+  AQP_CUDA(cudaMemsetAsync(lnnz, 0, sizeof(unsigned long long), st));
+  k_sellp_sort<<<(unsigned)nblk, 256, 0, st>>>(M.ptr, M.rows, perm, w, lnnz);
+  AQP_CUDA(cudaGetLastError());
+  AQP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, w, off, (int)(nw + 1), st));
+  unsigned long long ln = 0;
+  AQP_CUDA(cudaMemcpyAsync(&tot, off + nw, sizeof(tot), cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaMemcpyAsync(&ln, lnnz, sizeof(ln), cudaMemcpyDeviceToHost, st));
   AQP_CUDA(cudaStreamSynchronize(st));
-  if (tot <= M.nnz + M.nnz / 8 + 32) *total = tot;
+  const double short_nnz = (double)M.nnz - (double)ln;
+  if ((double)ln <= 0.05 * (double)M.nnz && (double)tot <= short_nnz * (1.0 + pad_p) + 32) {
+    *total = tot;
+    *sorted = true;
+  }
   return AQP_OK;
+}
+
+__global__ void k_fill_sellp(const int *__restrict__ ptr, const int *__restrict__ idx, const double *__restrict__ val,
+                             int rows, const uint8_t *__restrict__ perm, const int64_t *__restrict__ off, int *sidx,
+                             double *sval) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= rows) return;
+  const int64_t r = (p & ~(int64_t)255) + perm[p];
+  const int b = ptr[r], e = ptr[r + 1];
+  if (e - b > kThreadRowMax) return;  // long rows stay in the CSR
+  const int64_t base = off[p >> 5] + (p & 31);
+  for (int k = 0; k < e - b; ++k) {
+    sidx[base + 32 * k] = idx[b + k];
+    sval[base + 32 * k] = val[b + k];
+  }
 }
 
 // ---------------------------------------------------------------- diagonal split (DevCsr::diag)
@@ -488,7 +556,8 @@ void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz) {
   s.seg_cap = nnz / kSegNnz + nnz / kTileNnz + 2;  // each long row adds at most one partial segment
   s.seg_part = (double *)b.take(2 * s.seg_cap * sizeof(double));
   s.seg_ticket = (unsigned *)b.take(s.seg_cap * sizeof(unsigned));
-  s.sell_off = (int64_t *)b.take((rows / 32 + 2) * sizeof(int64_t));
+  s.sell_off = (int64_t *)b.take(((rows + 255) / 256 * 8 + 2) * sizeof(int64_t));
+  s.sell_perm = (uint8_t *)b.take(std::max<int64_t>(rows, 1));
 }
 
 // Upload an int64 CSR (device pointers) into int32 storage and plan it.
@@ -679,6 +748,11 @@ int aqp_ctx_create(int device, void *stream, aqp_ctx **out) {
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  const int rc = xfer_init(device);  // the staged-copy pool (aqp_xfer.cu), once per process
+  if (rc != AQP_OK) {
+    delete c;
+    return rc;
+  }
   *out = c;
   return AQP_OK;
 }
@@ -792,6 +866,7 @@ static void layout_problem(Bump &b, const aqp_problem_desc *d, aqp_problem *p) {
   p->cone_y = (int8_t *)b.take(std::max<int64_t>(m, 1));
   p->recc_s = (int8_t *)b.take(std::max<int64_t>(m, 1));
   p->bad = (int *)b.take(64);
+  p->setup_scratch = b.take(256);
 }
 
 static int check_shard(const aqp_problem_desc *d) {
@@ -1053,7 +1128,8 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
     for (int i = 0; i < 5; ++i) {
       if (i == 2 && d->quad_kind == AQP_QUAD_DIAGONAL) continue;
       if (i >= 3 && (d->quad_kind != AQP_QUAD_SPARSE_LOW_RANK || p->r_dense)) continue;
-      rc = plan_sell(ctx, *mats[i], stores[i]->sell_off, sc, &p->sell_total[i]);
+      rc = plan_sell(ctx, *mats[i], stores[i]->sell_off, stores[i]->sell_perm, i == 1, sc, &p->sell_total[i],
+                     &p->sell_sorted[i]);
       if (rc) return cleanup(rc);
     }
   }
@@ -1107,13 +1183,27 @@ int aqp_problem_attach_sell(aqp_problem *p, void *buf, size_t bytes) {
     at += align256((size_t)tot * 4);
     double *sval = reinterpret_cast<double *>(at);
     at += align256((size_t)tot * 8);
-    k_fill_sell<<<(M.rows + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, M.val, M.rows, stores[i]->sell_off, sidx, sval);
+    if (p->sell_sorted[i]) {
+      k_fill_sellp<<<(M.rows + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, M.val, M.rows, stores[i]->sell_perm,
+                                                         stores[i]->sell_off, sidx, sval);
+      // the SELL-P kernel runs one block per 256 rows and sums long rows itself
+      M.sell_perm = stores[i]->sell_perm;
+      M.uniform = 1;
+      M.nitems = (M.rows + kThreads - 1) / kThreads;
+      M.smem_bytes = 0;
+    } else {
+      k_fill_sell<<<(M.rows + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, M.val, M.rows, stores[i]->sell_off, sidx,
+                                                        sval);
+    }
     AQP_CUDA(cudaGetLastError());
     M.sell_off = stores[i]->sell_off;
     M.sell_idx = sidx;
     M.sell_val = sval;
   }
   AQP_CUDA(cudaStreamSynchronize(st));
+  p->info.a_items = p->A.nitems;
+  p->info.at_items = p->At.nitems;
+  p->info.q_items = p->Q.nitems;
   return AQP_OK;
 }
 

@@ -55,11 +55,15 @@ __global__ void k_scale_csr(DevCsr M, const double *__restrict__ rs, const doubl
 }
 
 // the SELL-32 copy of a uniform plan's matrix (DevCsr::sell_*) follows its CSR
+// (thread = SELL position: natural SELL position p is row p; SELL-P position
+// p is row (p & ~255) + sell_perm[p], and long rows are not in the slices)
 __global__ void k_scale_sell(DevCsr M, const double *__restrict__ rs, const double *__restrict__ cs) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= M.rows || !M.sell_val) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= M.rows || !M.sell_val) return;
+  const int r = M.sell_perm ? (p & ~255) + M.sell_perm[p] : p;
   const int len = M.ptr[r + 1] - M.ptr[r];
-  const int64_t base = M.sell_off[r >> 5] + (r & 31);
+  if (M.sell_perm && len > kThreadRowMax) return;
+  const int64_t base = M.sell_off[p >> 5] + (p & 31);
   double *sval = const_cast<double *>(M.sell_val);
   const double s = rs[r];
   for (int k = 0; k < len; ++k) sval[base + 32 * k] = sval[base + 32 * k] * s * cs[M.sell_idx[base + 32 * k]];

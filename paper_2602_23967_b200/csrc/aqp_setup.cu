@@ -46,6 +46,22 @@ __device__ __forceinline__ void max_nonneg(unsigned long long *slot, double v) {
   atomicMax(slot, (unsigned long long)__double_as_longlong(v));
 }
 
+// thread-local max of non-negative doubles as bit patterns; one atomic per
+// warp at the end (a per-element atomic on one address serialises in L2:
+// ~0.15 s over C5's 1e8 bounds)
+struct MaxAcc {
+  unsigned long long b = 0;
+  __device__ __forceinline__ void add(double v) {
+    if (v > 0.0) b = max(b, (unsigned long long)__double_as_longlong(v));
+  }
+  __device__ __forceinline__ void flush(unsigned long long *slot) {
+    unsigned long long x = b;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if ((threadIdx.x & 31) == 0 && x) atomicMax(slot, x);
+  }
+};
+
 __device__ __forceinline__ bool finite(double v) { return isfinite(v); }
 
 // _check_bounds (model.py:168-178) + finite_bound_scale (certify.py:54-60)
@@ -53,16 +69,16 @@ __global__ void k_setup_bounds(const double *__restrict__ lo, const double *__re
                                int64_t base, int *nan_flag, int *winf_flag, unsigned long long *first_inv,
                                unsigned long long *scale) {
   int nan_l = 0, winf_l = 0;
+  MaxAcc mx;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double l = lo[i], h = hi[i];
     nan_l |= isnan(l) || isnan(h);
     winf_l |= (isinf(l) && l > 0.0) || (isinf(h) && h < 0.0);
     if (l > h) atomicMin(first_inv, (unsigned long long)(base + i));
-    if (scale) {
-      if (finite(l)) max_nonneg(scale, fabs(l));
-      if (finite(h)) max_nonneg(scale, fabs(h));
-    }
+    if (finite(l)) mx.add(fabs(l));
+    if (finite(h)) mx.add(fabs(h));
   }
+  if (scale) mx.flush(scale);
   if (__syncthreads_or(nan_l) && threadIdx.x == 0) *nan_flag = 1;
   if (__syncthreads_or(winf_l) && threadIdx.x == 0) *winf_flag = 1;
 }
@@ -70,36 +86,41 @@ __global__ void k_setup_bounds(const double *__restrict__ lo, const double *__re
 // non-finite flag of an array, and optionally its max |v|
 __global__ void k_setup_finite(const double *__restrict__ v, int64_t n, int *bad, unsigned long long *absmax) {
   int b = 0;
+  MaxAcc mx;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double x = v[i];
     b |= !finite(x);
-    if (absmax) max_nonneg(absmax, fabs(x));
+    mx.add(fabs(x));
   }
+  if (absmax) mx.flush(absmax);
   if (__syncthreads_or(b) && threadIdx.x == 0) *bad = 1;
 }
 
 // max(initial=0) of a vector (diag_bound of the diagonal / sparse kinds)
 __global__ void k_setup_max(const double *__restrict__ v, int64_t n, unsigned long long *out) {
+  MaxAcc mx;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    max_nonneg(out, v[i]);
+    mx.add(v[i]);
+  mx.flush(out);
 }
 
 // SparseQuad.inf_norm_bound (linalg.py:218-220) over the full symmetric rows
 // of this problem; also the non-finite flag of Q's values.
 __global__ void k_setup_qrows(DevCsr Q, const double *__restrict__ pdiag, int *bad, unsigned long long *out) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= Q.rows) return;
+  const int r0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = r0 < Q.rows;
+  const int r = live ? r0 : 0;
   const int rg = r + Q.row_off;
   double col = 0.0, row = 0.0;
   bool nonfin = false;
-  const int b = Q.ptr[r], e = Q.ptr[r + 1];
+  const int b = Q.ptr[r], e = live ? Q.ptr[r + 1] : b;
   int k = b;
   for (; k < e && Q.idx[k] < rg; ++k) {  // mirrored part: column rg of U, ascending rows
     const double v = Q.val[k];
     nonfin |= !finite(v);
     col += fabs(v);
   }
-  if (Q.diag) {  // split diagonal (DevCsr::diag): U_ii, last of the column, first of the row
+  if (Q.diag && live) {  // split diagonal (DevCsr::diag): U_ii, last of the column, first of the row
     const double d = Q.diag[r];
     nonfin |= !finite(d);
     col += fabs(d);
@@ -112,7 +133,9 @@ __global__ void k_setup_qrows(DevCsr Q, const double *__restrict__ pdiag, int *b
     row += fabs(v);
   }
   if (nonfin) *bad = 1;
-  max_nonneg(out, row + col - fabs(pdiag[r]));
+  MaxAcc mx;
+  if (live) mx.add(row + col - fabs(pdiag[r]));
+  mx.flush(out);
 }
 
 // dense R (k x nl row-major): column abs sums and squares (bincount order:
@@ -120,18 +143,23 @@ __global__ void k_setup_qrows(DevCsr Q, const double *__restrict__ pdiag, int *b
 __global__ void k_setup_rdense_cols(const double *__restrict__ R, int k, int64_t nl, const double *__restrict__ pdiag,
                                     int *bad, unsigned long long *r_one, unsigned long long *dbound) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= nl) return;
+  const bool live = j < nl;
   double ca = 0.0, sq = 0.0;
   bool nonfin = false;
-  for (int i = 0; i < k; ++i) {
+  for (int i = 0; live && i < k; ++i) {
     const double v = R[(int64_t)i * nl + j];
     nonfin |= !finite(v);
     ca += fabs(v);
     sq += v * v;
   }
   if (nonfin) *bad = 1;
-  max_nonneg(r_one, ca);
-  max_nonneg(dbound, pdiag[j] + sq);
+  MaxAcc m1, m2;
+  if (live) {
+    m1.add(ca);
+    m2.add(pdiag[j] + sq);
+  }
+  m1.flush(r_one);
+  m2.flush(dbound);
 }
 
 // dense R row abs sums: one block per row; the block stages 2048 entries of
@@ -159,18 +187,23 @@ __global__ void __launch_bounds__(256) k_setup_rdense_rows(const double *__restr
 __global__ void k_setup_csr_rows(DevCsr M, const double *__restrict__ pdiag, int *bad, unsigned long long *absmax,
                                  unsigned long long *dbound) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= M.rows) return;
+  const bool live = r < M.rows;
   double a = 0.0, sq = 0.0;
   bool nonfin = false;
-  for (int k = M.ptr[r]; k < M.ptr[r + 1]; ++k) {
+  for (int k = live ? M.ptr[r] : 0, e = live ? M.ptr[r + 1] : 0; k < e; ++k) {
     const double v = M.val[k];
     nonfin |= !finite(v);
     a += fabs(v);
     sq += v * v;
   }
   if (nonfin && bad) *bad = 1;
-  max_nonneg(absmax, a);
-  if (pdiag) max_nonneg(dbound, pdiag[r] + sq);
+  MaxAcc m1, m2;
+  if (live) {
+    m1.add(a);
+    if (pdiag) m2.add(pdiag[r] + sq);
+  }
+  m1.flush(absmax);
+  if (pdiag) m2.flush(dbound);
 }
 
 inline int grid_n(int64_t n) {
@@ -198,8 +231,8 @@ int aqp_problem_setup_info(aqp_problem *p, aqp_setup_info *out) {
   if (!p || !out) return fail(AQP_EINVAL, "NULL argument");
   cudaStream_t st = p->ctx->stream;
   AQP_CUDA(cudaSetDevice(p->ctx->device));
-  SetupDev *d = nullptr;
-  AQP_CUDA(cudaMallocAsync(&d, sizeof(SetupDev), st));
+  static_assert(sizeof(SetupDev) <= 256, "setup_scratch holds SetupDev");
+  SetupDev *d = static_cast<SetupDev *>(p->setup_scratch);
   AQP_CUDA(cudaMemsetAsync(d, 0, sizeof(SetupDev), st));
   AQP_CUDA(cudaMemsetAsync(&d->var_inv, 0xff, 2 * sizeof(unsigned long long), st));
   const int64_t nl = p->n1 - p->n0, ml = p->m1 - p->m0;
@@ -246,7 +279,6 @@ int aqp_problem_setup_info(aqp_problem *p, aqp_setup_info *out) {
   AQP_CUDA(cudaGetLastError());
   SetupDev h;
   AQP_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
-  AQP_CUDA(cudaFreeAsync(d, st));
   AQP_CUDA(cudaStreamSynchronize(st));
   out->var_nan = h.var_nan;
   out->var_wrong_inf = h.var_winf;

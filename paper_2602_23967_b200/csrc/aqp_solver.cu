@@ -1410,6 +1410,7 @@ cudaError_t add_node(cudaGraph_t g, GNode &last, unsigned grid, K fn, A... args)
 
 template <class Op>
 cudaError_t node_spmv(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
+  if (M.sell_perm) return add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_sellp_op<Op>, M, op, gr);
   if (M.uniform) return add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_op<Op, true>, M, op, gr);
   return add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M, op, gr);
 }
@@ -1421,9 +1422,10 @@ cudaError_t node_elem(cudaGraph_t g, GNode &last, int64_t n, const Op &op, GridR
 // SPLIT ops: the main launch followed by its one-block fold/finalize
 template <class Op>
 cudaError_t node_spmv_fin(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
-  cudaError_t e = M.uniform ? add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_op<Op, true>, M, op, gr)
-                            : add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M,
-                                            op, gr);
+  cudaError_t e = M.sell_perm ? add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_sellp_op<Op>, M, op, gr)
+                   : M.uniform  ? add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_op<Op, true>, M, op, gr)
+                                : add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M,
+                                                op, gr);
   if (e != cudaSuccess) return e;
 #if AQP_FOLD_CLUSTER
   return add_node_cfg(g, last, (unsigned)kFoldCtas, (unsigned)kFoldThreads, 0u, fin_ctrl_cl<Op>, op, gr,
@@ -1452,7 +1454,9 @@ cudaError_t node_barrier(cudaGraph_t g, GNode &last, GridRed gr) {
 
 template <class Op>
 cudaError_t run_spmv(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
-  if (M.uniform)
+  if (M.sell_perm)
+    spmv_sellp_op<Op><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
+  else if (M.uniform)
     spmv_op<Op, true><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
   else
     spmv_op<Op><<<M.nitems, kThreads, M.smem_bytes, st>>>(M, op, gr);
@@ -1465,7 +1469,9 @@ cudaError_t run_elem(cudaStream_t st, int64_t n, const Op &op, GridRed gr) {
 }
 template <class Op>
 cudaError_t run_spmv_fin(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
-  if (M.uniform)
+  if (M.sell_perm)
+    spmv_sellp_op<Op><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
+  else if (M.uniform)
     spmv_op<Op, true><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
   else
     spmv_op<Op><<<M.nitems, kThreads, M.smem_bytes, st>>>(M, op, gr);

@@ -5,7 +5,7 @@
 // cudaMemcpy runs at ~10 GB/s H2D and ~4.5 GB/s D2H on the B200 box; this
 // engine stages through pinned buffers instead: T host threads each own two
 // pinned chunks and a stream, and pipeline memcpy(host <-> pinned) against
-// the DMA of the other chunk (measured 45 GB/s H2D with 8 threads x 32 MB,
+// the DMA of the other chunk (measured 45 GB/s H2D with 8 threads x 16-32 MB,
 // scripts/h2d_probe.py).  The pinned pool is allocated once per process
 // (cudaHostAlloc synchronises the device, so never per call) and reused; a
 // mutex serialises transfers (one pool).
@@ -27,7 +27,7 @@ namespace aqp {
 namespace {
 
 constexpr int kXferThreads = 8;
-constexpr size_t kXferChunk = size_t(32) << 20;  // bytes per pinned buffer
+constexpr size_t kXferChunk = size_t(32) << 20;  // bytes per pinned buffer (16 MB: 33 GB/s)
 constexpr size_t kStagedMin = size_t(8) << 20;
 
 struct XferPool {
@@ -49,10 +49,9 @@ XferPool &pool() {
 }
 
 int pool_ready(XferPool &p, int device) {
-  if (!p.ready) {
+  if (!p.ready) {  // (pinning from several threads at once measured slower: driver contention)
     for (int t = 0; t < kXferThreads; ++t)
-      for (int j = 0; j < 2; ++j)
-        AQP_CUDA(cudaHostAlloc(&p.buf[t][j], kXferChunk, cudaHostAllocPortable));
+      for (int j = 0; j < 2; ++j) AQP_CUDA(cudaHostAlloc(&p.buf[t][j], kXferChunk, cudaHostAllocPortable));
     p.ready = true;
   }
   if (device < 0 || device >= 64) return fail(AQP_EINVAL, "device id out of range");
@@ -106,6 +105,14 @@ void xfer_worker(XferPool &p, int device, int t, char *dev, char *host, size_t b
 }
 
 }  // namespace
+
+// Allocate the pool and the device's streams now (aqp_ctx_create: runtime
+// initialisation, not per solve -- the 512 MB of pinning takes ~0.25 s).
+int xfer_init(int device) {
+  XferPool &p = pool();
+  std::lock_guard<std::mutex> lock(p.mu);
+  return pool_ready(p, device);
+}
 
 // Synchronous bulk copy on `device`; the caller orders it against its own
 // stream (H2D: the destination is not in use; D2H: the source is complete).
