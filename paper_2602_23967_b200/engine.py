@@ -375,7 +375,7 @@ def _scaled_diag_bound(quad, d: np.ndarray) -> float:
 
 def solve(problem, params: Optional[SolverParams] = None, progress: Optional[ProgressCallback] = None,
           device: int = 0, monitor: Optional[Callable[[int, int], None]] = None, group=None,
-          marks: Optional[Sequence[int]] = None) -> SolveResult:
+          marks: Optional[Sequence[int]] = None, stats: Optional[dict] = None) -> SolveResult:
     """Run until optimality, an infeasibility certificate, or a limit
     (engine.py:339-498).  ``problem`` may be this package's QpProblem or the
     reference's (rebuilt field by field).
@@ -394,9 +394,16 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
 
     ``group`` (extension, shard.PeerGroup): solve this problem row-sharded
     with the group's other ranks; every rank calls solve
-    with the same problem and params and gets the same result."""
+    with the same problem and params and gets the same result.
+
+    ``stats`` (extension): a dict that receives branch counters of the loop --
+    ``halts`` (device windows stopped by a non-finite move, the overflow
+    rollback of engine.py:407-417) and ``rollbacks_divergence``
+    (engine.py:484-487)."""
     params = params or SolverParams()
     ph = _Phases()
+    counters = stats if stats is not None else {}
+    counters.update(halts=0, rollbacks_divergence=0)
     problem = QpProblem.from_any(problem)
     validate_dims(problem)  # the data checks of validate() run on the device (_Run)
     ph("validate")
@@ -488,6 +495,7 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
                 monitor(n_outer, n_inner)
         if sc.halted:
             # engine.py:407-417: overflow inside the round
+            counters["halts"] += 1
             sol.rollback()
             rs.round += 1
             rs.theta = rs.theta / 2.0 if rs.theta >= THETA_BACKOFF_FLOOR else 0.0
@@ -541,6 +549,7 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
         elif stall_checks >= STALL_CHECKS:
             probe_until = n_outer + rp.max_round_len
         elif not math.isfinite(kkt) or kkt > DIVERGENCE_FACTOR * rs.best_residual_round_start:
+            counters["rollbacks_divergence"] += 1
             rollback_round()
             run.mark_cert()
         elif rp.enabled and restart_decision(k_now, rs, kkt, params):

@@ -51,6 +51,7 @@ GOLDENS = [
     ("c2:1e4:5e3:0", "ref_c2_1e4_5e3_0.json"),
     ("c3:2e3:100:0", "ref_c3_2e3_100_0.json"), ("c3:2e4:100:0", "ref_c3_2e4_100_0.json"),
     ("c5:5e4:500:0", "ref_c5_5e4_500_0.json"), ("c5:5e4:500:0:diag", "ref_c5_5e4_500_0_diag.json"),
+    ("c5:5e5:500:0", "ref_c5_5e5_500_0.json"),  # C5/100 (reference: 674 s on one core)
     ("rqp:300:150:sparse:0.05:7", "ref_rqp_300_150_sparse_0.05_7.json"),
     ("rqp:300:150:low_rank:0.05:3", "ref_rqp_300_150_low_rank_0.05_3.json"),
     ("rqp:500:300:diagonal:0.02:5", "ref_rqp_500_300_diagonal_0.02_5.json"),
@@ -271,3 +272,33 @@ def test_opt_in_scaling_keeps_status_and_objective(cuda, spec, fname, scaling):
         assert abs(res.report.primal_objective - g["objective"]) <= 1e-6 * max(1.0, abs(g["objective"]))
     else:
         assert res.certificate is not None
+
+
+@pytest.mark.parametrize("fname", ["ref_rb_theta0.9_rqp_300_150_sparse_0.05_7.json",
+                                   "ref_rb_theta0.99_rqp_300_150_sparse_0.05_7.json",
+                                   "ref_rb_eta1000_rqp_300_150_sparse_0.05_7.json"])
+def test_rollback_branches_match_reference(cuda, fname):
+    """The two rollback branches of the reference loop, forced by parameters
+    and recorded from the reference with per-branch call counts
+    (oracle/run_reference.py): a large Halpern reflection theta diverges and
+    is rolled back to the round anchor with theta halved (engine.py:484-487,
+    303-319) until it converges; a 1000x step scale overflows inside the
+    device window (the device halt flag, engine.py:407-417) and diverges at
+    checks, until the iteration limit."""
+    g = golden(fname)
+    prm = SolverParams(eps_tol=g["eps_tol"], iter_limit=g["iter_limit"], **g["params"])
+    stats = {}
+    trace = []
+    res = solve(instances.build(g["spec"]), prm, stats=stats,
+                progress=lambda it, rep, om, rnd: trace.append((it, rnd)))
+    ref_rb = g["rollbacks"]
+    assert res.status.value == g["status"]
+    assert stats["halts"] == ref_rb["overflow"] and stats["rollbacks_divergence"] == ref_rb["divergence"]
+    assert (stats["halts"] > 0) == (ref_rb["overflow"] > 0)  # the device halt flag fired iff the reference overflowed
+    if g["status"] == "optimal":
+        assert_parity(res, g["status"], g["outer"], g["objective"], g["eps_tol"])
+        assert res.restarts == g["restarts"]
+    else:
+        assert res.outer_iterations == g["outer"]
+    # the round counter at every certification point follows the reference's
+    assert [r for _, r in trace] == [t[5] for t in g["trace"]]
