@@ -9,6 +9,8 @@ Specs (all seeded, all built by ``paper_2602_23967_b200.generators``):
     c4u:<n>:<seed> / c4i:<n>:<seed>   infeasible_pair(n, seed) [0] / [1]           (config 4)
     c4ur / c4ir                        same on SURVEY.md's random_qp base
     c5:<n>:<w>:<seed>[:diag]  banded_qp(n, n, half_width=w, seed, diagonal_q)       (config 5 / twins)
+    qps:<path>                a QPS file read by this repo's reader (io.parse_qps); the
+                              reference golden of the same file uses the reference's reader
 """
 
 from __future__ import annotations
@@ -32,6 +34,16 @@ def build(spec: str):
         base = "random_qp" if kind.endswith("r") else "diagonal"
         pair = g.infeasible_pair(int(float(parts[1])), seed=int(parts[2]), base=base)
         return pair[0] if kind.startswith("c4u") else pair[1]
+    if kind == "qps":
+        from paper_2602_23967_b200 import io
+
+        import os
+
+        path = spec.split(":", 1)[1]
+        if not os.path.isabs(path):  # relative to the repo root
+            path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), path)
+        with open(path) as f:
+            return io.parse_qps(f.read()).problem
     if kind == "c5":
         diag = len(parts) > 4 and parts[4] == "diag"
         n = int(float(parts[1]))

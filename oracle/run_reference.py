@@ -63,7 +63,11 @@ def main(argv=None):
     ref_engine._rollback_round = counted
     t0 = time.time()
     ours = instances.build(args.spec)
-    prob = refbridge.to_reference(ours, aq)
+    if args.spec.startswith("qps:"):  # the reference's own reader on the same file
+        with open(args.spec.split(":", 1)[1]) as f:
+            prob = aq.parse_qps(f.read()).problem
+    else:
+        prob = refbridge.to_reference(ours, aq)
     gen_s = time.time() - t0
     trace = []
 

@@ -52,6 +52,9 @@ GOLDENS = [
     ("c3:2e3:100:0", "ref_c3_2e3_100_0.json"), ("c3:2e4:100:0", "ref_c3_2e4_100_0.json"),
     ("c5:5e4:500:0", "ref_c5_5e4_500_0.json"), ("c5:5e4:500:0:diag", "ref_c5_5e4_500_0_diag.json"),
     ("c5:5e5:500:0", "ref_c5_5e5_500_0.json"),  # C5/100 (reference: 674 s on one core)
+    # a real QPS file (ranges, free rows, negative UP, FX/MI/PL, QMATRIX) read by
+    # this repo's reader; the golden is the reference solving its own parse
+    ("qps:tests/golden/qps_mixed_400.qps", "ref_qps_mixed_400.json"),
     ("rqp:300:150:sparse:0.05:7", "ref_rqp_300_150_sparse_0.05_7.json"),
     ("rqp:300:150:low_rank:0.05:3", "ref_rqp_300_150_low_rank_0.05_3.json"),
     ("rqp:500:300:diagonal:0.02:5", "ref_rqp_500_300_diagonal_0.02_5.json"),

@@ -2,6 +2,8 @@
 trip, and parity with the reference's own JSON and QPS readers/writers
 (``aq/serialize.py``, ``aq/qps.py``) run from oracle/_ref."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -212,3 +214,33 @@ def test_qps_errors_match_reference(k):
 def test_low_rank_has_no_qps_form():
     with pytest.raises(ValueError):
         aqio.write_qps(instances.build("rqp:20:12:low_rank:0.3:5"))
+
+
+QPS_FIXTURE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "qps_mixed_400.qps")
+
+
+def test_qps_fixture_is_the_generator_output():
+    """tests/golden/qps_mixed_400.qps is exactly oracle/gen_qps_fixture.py's output."""
+    import gen_qps_fixture
+
+    with open(QPS_FIXTURE) as f:
+        assert f.read() == gen_qps_fixture.build()
+
+
+@needs_ref
+def test_qps_fixture_parses_like_reference():
+    """The real-instance parity file (every reader convention): our reader and
+    the reference's give the same problem, bit for bit."""
+    from anchorqp import qps as rq
+
+    text = open(QPS_FIXTURE).read()
+    ours, theirs = aqio.parse_qps(text), rq.parse_qps(text)
+    assert ours.objective_constant == theirs.objective_constant == 12.5
+    same_problem(ours.problem, theirs.problem)
+    p = ours.problem
+    lo, hi = p.con_bounds.lower, p.con_bounds.upper
+    assert np.sum(np.isfinite(lo) & np.isfinite(hi) & (lo < hi)) >= 30  # ranged rows
+    assert np.sum(~np.isfinite(lo) & ~np.isfinite(hi)) == 2             # the two free N rows
+    vlo, vhi = p.var_bounds.lower, p.var_bounds.upper
+    assert np.any(~np.isfinite(vlo) & np.isfinite(vhi) & (vhi < 0))     # negative UP dropped the lower bound
+    assert np.any(vlo == vhi)                                           # FX
