@@ -180,6 +180,9 @@ __device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *
 #ifndef AQP_GATHER_BATCH
 #define AQP_GATHER_BATCH 4
 #endif
+#ifndef AQP_SELL_BATCH  // nonzeros per load batch on the SELL paths
+#define AQP_SELL_BATCH AQP_GATHER_BATCH
+#endif
 
 // UNIFORM: the plan is all THREAD items over [256 b, 256 b + 256) (the common
 // case of short-row matrices, e.g. every C2 pass); the instantiation then
@@ -231,20 +234,20 @@ __device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, c
         // SELL-32: the warp's k-th nonzeros are contiguous (coalesced loads)
         const int len = e - b;
         const int64_t base = __ldg(M.sell_off + (r >> 5)) + (r & 31);
-        for (int k = 0; k < len; k += AQP_GATHER_BATCH) {
-          int cc[AQP_GATHER_BATCH];
-          double pv[AQP_GATHER_BATCH];
+        for (int k = 0; k < len; k += AQP_SELL_BATCH) {
+          int cc[AQP_SELL_BATCH];
+          double pv[AQP_SELL_BATCH];
 #pragma unroll
-          for (int u = 0; u < AQP_GATHER_BATCH; ++u) {
+          for (int u = 0; u < AQP_SELL_BATCH; ++u) {
             const bool in = k + u < len;
             cc[u] = in ? __ldg(M.sell_idx + base + 32 * (k + u)) : 0;
             pv[u] = in ? __ldg(M.sell_val + base + 32 * (k + u)) : 0.0;
           }
 #pragma unroll
-          for (int u = 0; u < AQP_GATHER_BATCH; ++u)
+          for (int u = 0; u < AQP_SELL_BATCH; ++u)
             if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);
 #pragma unroll
-          for (int u = 0; u < AQP_GATHER_BATCH; ++u) {
+          for (int u = 0; u < AQP_SELL_BATCH; ++u) {
             if (k + u < len) {
               if (Op::SYM && cc[u] < rg) lo += pv[u]; else up += pv[u];
             }
@@ -414,20 +417,20 @@ __device__ __forceinline__ void spmv_sellp_block(const DevCsr &M, const Op &o, R
     double lo = 0.0, up = 0.0;
     if (Op::SYM && M.diag) up = __ldg(M.diag + r) * o.gather(rg);
     const int64_t base = __ldg(M.sell_off + (rn >> 5)) + (rn & 31);
-    for (int k = 0; k < len; k += AQP_GATHER_BATCH) {
-      int cc[AQP_GATHER_BATCH];
-      double pv[AQP_GATHER_BATCH];
+    for (int k = 0; k < len; k += AQP_SELL_BATCH) {
+      int cc[AQP_SELL_BATCH];
+      double pv[AQP_SELL_BATCH];
 #pragma unroll
-      for (int u = 0; u < AQP_GATHER_BATCH; ++u) {
+      for (int u = 0; u < AQP_SELL_BATCH; ++u) {
         const bool in = k + u < len;
         cc[u] = in ? __ldg(M.sell_idx + base + 32 * (k + u)) : 0;
         pv[u] = in ? __ldg(M.sell_val + base + 32 * (k + u)) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < AQP_GATHER_BATCH; ++u)
+      for (int u = 0; u < AQP_SELL_BATCH; ++u)
         if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);
 #pragma unroll
-      for (int u = 0; u < AQP_GATHER_BATCH; ++u) {
+      for (int u = 0; u < AQP_SELL_BATCH; ++u) {
         if (k + u < len) {
           if (Op::SYM && cc[u] < rg) lo += pv[u]; else up += pv[u];
         }

@@ -157,13 +157,25 @@ struct Combine {
   }
 };
 
+// resident 256-thread blocks per SM the hot passes' register budgets target
+// (A/B knobs, scripts/build_variants.sh)
+#ifndef AQP_P1_BLOCKS
+#define AQP_P1_BLOCKS 6
+#endif
+#ifndef AQP_GRAD_BLOCKS
+#define AQP_GRAD_BLOCKS 6
+#endif
+#ifndef AQP_P2_BLOCKS
+#define AQP_P2_BLOCKS 6
+#endif
+
 // ================================================================ iteration ops
 // P1 (BB path): lin = c + A'y ; x0 = clamp(x)
 struct OpP1Bb {
   static constexpr int NS = 0, NM = 0;
   static constexpr bool SYM = false, FINAL = false;
   static constexpr bool ROWIN_LATE = true;
-  static constexpr int UNIFORM_BLOCKS = 6;
+  static constexpr int UNIFORM_BLOCKS = AQP_P1_BLOCKS;
   SV v;
   const double *y;
   const double *x;
@@ -241,7 +253,7 @@ struct OpGrad {
   static constexpr int NS = INIT ? 4 : 7, NM = 0;
   static constexpr bool SYM = true, FINAL = true, SPLIT = true;
   static constexpr bool ROWIN_LATE = true;   // see aqp_kernels.cuh RowInLateOf
-  static constexpr int UNIFORM_BLOCKS = 6;
+  static constexpr int UNIFORM_BLOCKS = AQP_GRAD_BLOCKS;
   SV v;
   const double *xt, *cen, *xo, *go;
   double *gt;
@@ -462,7 +474,7 @@ struct OpP2 {
   // measured (scripts/p2_ab.sh): late epilogue loads at 6 blocks/SM take the
   // C5 dual pass from 2.53 to 2.04 ms and cost C2 2 us (once per outer iteration)
   static constexpr bool ROWIN_LATE = true;
-  static constexpr int UNIFORM_BLOCKS = 6;
+  static constexpr int UNIFORM_BLOCKS = AQP_P2_BLOCKS;
   SV v;
   const double *y, *yprev;
   double *ynew;

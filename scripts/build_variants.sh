@@ -8,7 +8,7 @@ FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++1
 while [ $# -gt 0 ]; do
   name=$1; defs=$2; shift 2
   objs=""
-  for src in aqp_problem aqp_solver aqp_registry aqp_scale; do
+  for src in aqp_problem aqp_solver aqp_registry aqp_scale aqp_xfer aqp_setup; do
     /usr/local/cuda/bin/nvcc $FL $defs -c paper_2602_23967_b200/csrc/$src.cu -o build/vobj/${name}_$src.o &
     objs="$objs build/vobj/${name}_$src.o"
   done

@@ -16,8 +16,16 @@ p = build(name)
 gen = time.time() - t
 trace = []
 t = time.time()
-res = aq.solve(p, aq.SolverParams(eps_tol=1e-8, time_limit=tl, scaling=scaling),
-               progress=lambda k, rep, om, rd: trace.append((k, rep.kkt_max, om)))
+
+
+def progress(k, rep, om, rd):
+    trace.append((k, rep.kkt_max, om))
+    if len(trace) % 20 == 1:  # partial evidence survives a killed run
+        print(json.dumps({"outer": k, "kkt": rep.kkt_max, "omega": om, "round": rd, "s": round(time.time() - t, 1)}),
+              file=sys.stderr, flush=True)
+
+
+res = aq.solve(p, aq.SolverParams(eps_tol=1e-8, time_limit=tl, scaling=scaling), progress=progress)
 torch.cuda.synchronize()
 wall = time.time() - t
 print(json.dumps({"config": name, "scaling": scaling, "n": p.n, "m": p.m, "status": res.status.value, "outer": res.outer_iterations,
