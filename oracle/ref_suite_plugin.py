@@ -12,6 +12,9 @@ against this repo, through the two drop-in boundaries of INTEGRATION.md:
     PYTHONPATH=oracle/_ref:oracle:. python -m pytest oracle/_ref/tests -p ref_suite_plugin
 """
 
+import json
+import os
+
 import anchorqp
 import anchorqp.certify as rcert
 import anchorqp.engine as reng
@@ -22,7 +25,32 @@ import paper_2602_23967_b200 as b200
 from paper_2602_23967_b200 import errors as b200_errors
 from paper_2602_23967_b200 import kernels as b200_kernels
 
-rkern._BACKENDS["cuda"] = b200_kernels
+# which tests actually reach the B200 path (AQP_REF_SUITE_REPORT=<path>: a
+# per-session JSON summary): a test "reaches" it when it calls the routed
+# solve or a kernel of the "cuda" backend
+_hits = {"solve": False, "kernel": False}
+_records = []
+
+
+class _CountingBackend:
+    """The B200 kernel module as seen by the reference registry, counting calls."""
+
+    def __init__(self, mod):
+        self._mod = mod
+
+    def __getattr__(self, name):
+        f = getattr(self._mod, name)
+        if not callable(f):
+            return f
+
+        def counted(*a, **k):
+            _hits["kernel"] = True
+            return f(*a, **k)
+
+        return counted
+
+
+rkern._BACKENDS["cuda"] = _CountingBackend(b200_kernels)
 _reference_solve = reng.solve
 
 
@@ -59,6 +87,7 @@ def b200_solve(problem, params=None, progress=None):
                                              primal_objective=rep.primal_objective,
                                              dual_objective=rep.dual_objective, dual_slack=rep.dual_slack),
                      omega, rnd)
+    _hits["solve"] = True
     try:
         res = b200.solve(problem, params, cb)
     except b200_errors.SolverError as exc:
@@ -73,3 +102,30 @@ reng.solve = b200_solve
 def pytest_report_header(config):
     return ["reference suite routed to the B200 build: anchorqp.solve -> paper_2602_23967_b200.solve, "
             "kernel backend 'cuda' -> paper_2602_23967_b200.kernels"]
+
+
+def pytest_runtest_setup(item):
+    _hits["solve"] = _hits["kernel"] = False
+
+
+def pytest_runtest_logreport(report):
+    if report.when == "call":
+        _records.append({"test": report.nodeid, "outcome": report.outcome, "solve": _hits["solve"],
+                         "kernel": _hits["kernel"]})
+
+
+def pytest_sessionfinish(session, exitstatus):
+    path = os.environ.get("AQP_REF_SUITE_REPORT")
+    if not path:
+        return
+    passed = [r for r in _records if r["outcome"] == "passed"]
+    summary = {
+        "tests": len(_records), "passed": len(passed),
+        "passed_via_b200_solve": sum(r["solve"] for r in passed),
+        "passed_via_b200_kernels_only": sum(r["kernel"] and not r["solve"] for r in passed),
+        "passed_touching_b200": sum(r["solve"] or r["kernel"] for r in passed),
+        "passed_reference_python_only": sum(not (r["solve"] or r["kernel"]) for r in passed),
+        "records": _records,
+    }
+    with open(path, "w") as f:
+        json.dump(summary, f, indent=1)

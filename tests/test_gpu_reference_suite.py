@@ -24,8 +24,11 @@ EXPECTED_FAIL = {"oracle/_ref/tests/test_bench.py::TestHarness::test_parallel_ma
 
 @pytest.mark.skipif(not os.path.isdir(SUITE), reason="oracle/_ref/tests missing (run oracle/build_ref.sh)")
 def test_reference_suite_passes_on_b200(cuda):
+    report = os.path.join(ROOT, "build", "ref_suite_report.json")
+    os.makedirs(os.path.dirname(report), exist_ok=True)
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(ROOT, "oracle", "_ref"),
-                                                       os.path.join(ROOT, "oracle"), ROOT]))
+                                                       os.path.join(ROOT, "oracle"), ROOT]),
+               AQP_REF_SUITE_REPORT=report)
     out = subprocess.run([sys.executable, "-m", "pytest", "oracle/_ref/tests", "-p", "ref_suite_plugin", "-q",
                           "-rf", "-p", "no:cacheprovider"], cwd=ROOT, env=env, capture_output=True, text=True,
                          timeout=1200)
@@ -33,3 +36,10 @@ def test_reference_suite_passes_on_b200(cuda):
     summary = out.stdout.strip().splitlines()[-1]
     assert failed <= EXPECTED_FAIL, f"{summary}\n{out.stdout[-4000:]}"
     assert " passed" in summary and "error" not in summary, summary
+    # how many of the passing tests actually exercise the B200 build (the rest
+    # test the reference's own Python: model, QPS, certify internals ...)
+    import json
+
+    rep = json.load(open(report))
+    print({k: v for k, v in rep.items() if k != "records"})
+    assert rep["passed_via_b200_solve"] >= 30 and rep["passed_via_b200_kernels_only"] >= 10

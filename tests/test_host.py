@@ -24,7 +24,6 @@ from paper_2602_23967_b200 import (
 from paper_2602_23967_b200 import _native as nat
 from paper_2602_23967_b200 import certify, engine
 from paper_2602_23967_b200.errors import DimensionMismatch, InvertedBound, NonFiniteData
-from paper_2602_23967_b200.inner import InnerTolerance, update_tolerance
 
 INF = np.inf
 
@@ -97,15 +96,6 @@ def test_reference_objects_are_adopted():
 
 
 # ---------------------------------------------------------------- rules (reference tests/test_inner.py:127-152, test_engine.py:187-248)
-def test_tolerance_rule():
-    t = update_tolerance(InnerTolerance(1e-2), omega=1.0, tau=1.0, primal_move=1.0)
-    assert t.current == pytest.approx(5e-4)
-    assert update_tolerance(InnerTolerance(1e-2), 1.0, 1.0, 0.0).current == 1e-9
-    assert update_tolerance(InnerTolerance(1e-8), 1.0, 1.0, 1.0).current == 1e-8
-    with pytest.raises(ValueError):
-        InnerTolerance(0.0)
-
-
 def _round(base, last):
     return engine._Round(omega=1.0, eta=1.0, theta=0.0, best_residual_round_start=base, last_check_kkt=last)
 
