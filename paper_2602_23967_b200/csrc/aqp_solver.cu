@@ -155,6 +155,13 @@ struct Combine {
     if (use_prev) z = z + c3 * prev[i];
     return z;
   }
+  // the same on preloaded operands
+  __device__ __forceinline__ double apply(double w, double anc, double prev) const {
+    if (plain) return w;
+    double z = a * w + b * anc;
+    if (use_prev) z = z + c3 * prev;
+    return z;
+  }
 };
 
 // resident 256-thread blocks per SM the hot passes' register budgets target
@@ -452,15 +459,30 @@ struct OpXPost {
     znew = pick3(v.xs, 3 - ct->xcur - ct->xprev);
     cb.init(v);
   }
-  __device__ void elem(int64_t i, RedVals<1, 0> &acc) const {
-    const double p = xp[i], xk = x[i];
-    const double xb = 2.0 * p + (-1.0) * xk;
+  __device__ void elem(int64_t i, RedVals<1, 0> &acc) const { elem_in(i, load(i), acc); }
+  // batched (elem_op BATCH): 4 iterations' loads in flight per thread -- C5
+  // 0.60 -> see DESIGN.md; same elements in the same order per thread
+  static constexpr int BATCH = 4;
+  struct In {
+    double p, xk, anc, prev, blk;
+  };
+  __device__ In load(int64_t i) const {
+    In r;
+    r.p = xp[i];
+    r.xk = x[i];
+    r.anc = cb.plain ? 0.0 : v.anc_x[i];
+    r.prev = (!cb.plain && cb.use_prev) ? xprev[i] : 0.0;
+    r.blk = v.xblk[i];
+    return r;
+  }
+  __device__ void elem_in(int64_t i, const In &in, RedVals<1, 0> &acc) const {
+    const double xb = 2.0 * in.p + (-1.0) * in.xk;
     v.xbar[i] = xb;
     peer_put_halo(v.cm, 0, v.xbar, i, i + v.xoff, xb);
-    const double z = cb(p, v.anc_x, xprev, (int)i);
-    const double d = z - xk;
+    const double z = cb.apply(in.p, in.anc, in.prev);
+    const double d = z - in.xk;
     acc.s[0] += d * d;
-    v.xblk[i] += z;
+    v.xblk[i] = in.blk + z;
     znew[i] = z;
   }
   __device__ void finalize(const RedVals<1, 0> &t) const { x_iteration_end(v, t.s[0], v.ctrl->bb_t); }
@@ -1137,6 +1159,10 @@ struct OpPwScale {  // xbb[dst] = xbb[src] / sqrt(red[slot]); stop when the norm
     o = pick3(v.xbb, dst);
   }
   __device__ void elem(int64_t i, RedVals<0, 0> &) const { o[i] = x[i] / nrm; }
+  static constexpr int BATCH = 4;  // elem_op: 4 loads in flight per thread
+  using In = double;
+  __device__ double load(int64_t i) const { return x[i]; }
+  __device__ void elem_in(int64_t i, double xi, RedVals<0, 0> &) const { o[i] = xi / nrm; }
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
 
