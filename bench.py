@@ -230,13 +230,15 @@ def run_reference(args, world, rank):
     r = ref_sample(problem, args.warmup, args.steps, threads)
     value = r["inner"] / r["seconds"]
     line = base_line(args, args.gpus, value, 1e3 * r["seconds"], args.gpus > 1)
+    # the same config block as the GPU arm (same workload, range and params):
+    # how the reference executes is described in cpu_baseline
     line["config"] = config_block(problem, args, args.gpus, args.gpus > 1)
-    line["config"]["parallelism"] = "reference CPU solver (single-threaded Cython kernels; OpenBLAS threads)"
     line.update({
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "inner_iters/s", "cores": threads, "kind": r["kind"], **host_cpu(),
                          "sample": f"outer iterations [{args.warmup}, {args.warmup + args.steps}) of the C5 solve "
-                                   f"({r['inner']} BB iterations in {r['seconds']:.1f}s; backend {r['backend']}; "
+                                   f"({r['inner']} BB iterations in {r['seconds']:.1f}s; backend {r['backend']}: "
+                                   f"single-threaded Cython kernels, numpy/OpenBLAS with {threads} threads; "
                                    f"instance generation {gen_s:.0f}s, conversion {r.get('convert_seconds', 0):.0f}s "
                                    f"and initialisation {r.get('init_seconds') or 0:.0f}s untimed)"},
         "e2e": {"value": value, "unit": "inner_iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
