@@ -43,7 +43,6 @@ constexpr int kTileNnz = 2048;         // nonzeros staged per SpMV row-block (16
 constexpr int kSegNnz = 8192;          // nonzeros per block for a split long row
 constexpr int kThreadRowMax = 48;      // longest row handled one-thread-per-row
 constexpr int kMaxRed = 16;            // max reduction slots of one kernel
-constexpr int kTileSlots = 192;        // max per-SM tile ranges of a banded SpMV (%nsmid)
 
 // ---------------------------------------------------------------- scalar helpers
 // Reference semantics: _clip in _core.pyx:21-26 (lo first, then hi; NaN passes through)
@@ -430,13 +429,6 @@ struct DevCsr {
   // a shared-memory hand-off.  (Sorting within a warp only -- no block
   // barrier, natural slice widths -- measured slower: C5 A' 2.80 ms.)
   const uint8_t *sell_perm = nullptr;
-  // Banded matrices (every 256-row tile gathers from a short column window,
-  // e.g. C5's A, A' and Q): tiles are claimed per SM instead of by blockIdx
-  // (claim_tile), so the ~6 blocks resident on an SM walk one contiguous
-  // stretch of rows together and their gather windows overlap in that SM's
-  // L1.  tile_ctr: kTileSlots per-SM-range claim counters + the success
-  // ticket (self-resetting); null = blockIdx order.
-  unsigned *tile_ctr = nullptr;
   // full symmetric Q of a uniform plan: its diagonal moved out of the CSR into
   // diag[local row].  A row's upper sum starts with diag * x[row] -- the
   // diagonal is the first j >= i entry, so the order is unchanged -- and the

@@ -30,7 +30,6 @@ struct CsrStore {
   int64_t seg_cap = 0;
   int64_t *sell_off = nullptr;  // SELL-32 slice offsets (8 per 256-row block + 2), planned by plan_sell
   uint8_t *sell_perm = nullptr;  // SELL-P position -> row within its 256-row block (rows bytes)
-  unsigned *tile_ctr = nullptr;  // per-SM tile claim counters of a banded SpMV (kTileSlots + 1)
 };
 
 void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz);

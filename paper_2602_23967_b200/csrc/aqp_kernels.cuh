@@ -145,13 +145,11 @@ __device__ __forceinline__ void fold_partials(RedVals<NS, NM> &a, const double *
 // End of a reducing launch.  SPLIT: publish this block's partials and return
 // false.  Otherwise the last-block ticket: returns true in thread 0 of the
 // last block with the grid totals in `v`.
-// `slot`: this block's partial index (its tile: blockIdx.x, or the claimed
-// tile of a banded SpMV -- the fold order is tile order either way)
 template <int NS, int NM, bool SPLIT>
-__device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *smem, unsigned slot = 0xffffffffu) {
+__device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *smem) {
   constexpr int NT = NS + NM;
   __shared__ bool last;
-  if (slot == 0xffffffffu) slot = blockIdx.x;
+  const unsigned slot = blockIdx.x;
   if constexpr (NT > 0) block_reduce<NS, NM>(v, smem);
   if (threadIdx.x == 0) {
     const unsigned nb = gridDim.x;
@@ -395,11 +393,11 @@ __device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, c
 // thread map (so the same reductions) as the natural uniform path.
 template <class Op>
 __device__ __forceinline__ void spmv_sellp_block(const DevCsr &M, const Op &o, RedVals<Op::NS, Op::NM> &acc,
-                                                 double *sred, unsigned tile) {
+                                                 double *sred) {
   __shared__ double ssum[kThreads];
   __shared__ int lrow[kThreads];
   __shared__ int nlr;
-  const int blk = tile * kThreads, t = threadIdx.x;
+  const int blk = blockIdx.x * kThreads, t = threadIdx.x;
   const int rn = blk + t;  // epilogue row (= sorted position index)
   using RowIn = typename RowInOf<Op>::type;
   RowIn rin{};
@@ -468,53 +466,14 @@ __device__ __forceinline__ void spmv_sellp_block(const DevCsr &M, const Op &o, R
   }
 }
 
-// The tile this block runs (banded matrices, DevCsr::tile_ctr): tiles are
-// cut into one contiguous range per SM id (%nsmid, at most kTileSlots); a block claims the next tile of the
-// range of the SM it runs on, or -- once that range is done -- of the
-// following ranges (every block gets exactly one tile: grid = tiles).  The
-// block whose claim completes the grid resets the counters for the next
-// launch (no claim can be in flight then: every block has its tile).  Reads
-// only this kernel's counters, so it runs before griddepcontrol.wait.
-__device__ __forceinline__ unsigned claim_tile(unsigned *ctr) {
-  __shared__ unsigned s_tile;
-  if (threadIdx.x == 0) {
-    unsigned sm, nsm;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsm));
-    const unsigned T = gridDim.x, S = min(nsm, (unsigned)kTileSlots);  // one range per SM id
-    sm %= S;
-    unsigned tile = 0;
-    for (unsigned k = 0; k < S; ++k) {
-      const unsigned s = (sm + k) % S;
-      const unsigned lo = (unsigned)((uint64_t)T * s / S), hi = (unsigned)((uint64_t)T * (s + 1) / S);
-      if (hi == lo || *(volatile unsigned *)(ctr + s) >= hi - lo) continue;  // empty / (probably) done
-      const unsigned c = atomicAdd(ctr + s, 1u);
-      if (c < hi - lo) {
-        tile = lo + c;
-        break;
-      }
-    }
-    if (atomicAdd(ctr + kTileSlots, 1u) == T - 1) {  // the last claim of this launch
-      for (unsigned s = 0; s < S; ++s) ctr[s] = 0u;
-      ctr[kTileSlots] = 0u;
-      __threadfence();
-    }
-    s_tile = tile;
-  }
-  __syncthreads();
-  return s_tile;
-}
-
 template <class Op, bool UNIFORM = false>
 __global__ void __launch_bounds__(kThreads, UNIFORM ? UniformBlocksOf<Op>::value : AQP_SPMV_MIN_BLOCKS) spmv_op(DevCsr M, Op op, GridRed g) {
   constexpr int NS = Op::NS, NM = Op::NM;
   // static matrix data first: the plan item does not depend on the predecessor
   PlanItem it;
-  unsigned tile = blockIdx.x;
   if (UNIFORM || M.uniform) {
-    if (M.tile_ctr) tile = claim_tile(M.tile_ctr);
     it.kind = kItemThread;
-    it.row0 = tile * kThreads;
+    it.row0 = blockIdx.x * kThreads;
     it.row1 = min(it.row0 + kThreads, M.rows);
   } else {
     it = M.plan[blockIdx.x];
@@ -535,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? UniformBlocksOf<Op>::value
   spmv_item<Op, UNIFORM>(M, it, o, acc, sprod, scol, sred);
   pdl_trigger();
   if constexpr (Op::FINAL) {
-    if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred, tile)) o.finalize(acc);
+    if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred)) o.finalize(acc);
   }
 }
 
@@ -544,7 +503,6 @@ __global__ void __launch_bounds__(kThreads, UNIFORM ? UniformBlocksOf<Op>::value
 template <class Op>
 __global__ void __launch_bounds__(kThreads, UniformBlocksOf<Op>::value) spmv_sellp_op(DevCsr M, Op op, GridRed g) {
   constexpr int NS = Op::NS, NM = Op::NM;
-  const unsigned tile = M.tile_ctr ? claim_tile(M.tile_ctr) : blockIdx.x;
   pdl_wait();
   trace_mark(g, 0);
   if (op.skip()) return;
@@ -553,10 +511,10 @@ __global__ void __launch_bounds__(kThreads, UniformBlocksOf<Op>::value) spmv_sel
   __shared__ double sred[kWarps * kMaxRed];
   RedVals<NS, NM> acc;
   acc.zero();
-  spmv_sellp_block<Op>(M, o, acc, sred, tile);
+  spmv_sellp_block<Op>(M, o, acc, sred);
   pdl_trigger();
   if constexpr (Op::FINAL) {
-    if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred, tile)) o.finalize(acc);
+    if (grid_end<NS, NM, SplitOf<Op>::value>(acc, g, sred)) o.finalize(acc);
   }
 }
 

@@ -402,44 +402,6 @@ static int plan_sell(aqp_ctx *ctx, const DevCsr &M, int64_t *off, uint8_t *perm,
   return AQP_OK;
 }
 
-// widest column window of a 256-row tile (rows hold ascending columns)
-__global__ void k_tile_span(const int *__restrict__ ptr, const int *__restrict__ idx, int rows, int *span) {
-  __shared__ int lo, hi;
-  if (threadIdx.x == 0) {
-    lo = INT_MAX;
-    hi = -1;
-  }
-  __syncthreads();
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < rows) {
-    const int b = ptr[r], e = ptr[r + 1];
-    // the row's own index too: a split diagonal / the epilogue touch it
-    atomicMin(&lo, e > b ? min(idx[b], r) : r);
-    atomicMax(&hi, e > b ? max(idx[e - 1], r) : r);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && hi >= lo) atomicMax(span, hi - lo + 1);
-}
-
-// Banded matrix: every tile's column window <= kBandSpan and enough tiles
-// that SM-local tile order pays (DevCsr::tile_ctr).  AQP_TILE_ORDER=0: off.
-static int plan_tile_order(aqp_ctx *ctx, DevCsr &M, unsigned *ctr, int *dscratch) {
-  constexpr int kBandSpan = 16384;  // columns: 128 KB of gathered doubles, inside one SM's L1
-  M.tile_ctr = nullptr;
-  const char *e = getenv("AQP_TILE_ORDER");
-  if ((e && e[0] == '0') || !ctr || M.rows < 256 * 148 * 8 || M.nnz == 0) return AQP_OK;
-  cudaStream_t st = ctx->stream;
-  AQP_CUDA(cudaMemsetAsync(dscratch, 0, sizeof(int), st));
-  k_tile_span<<<(M.rows + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, M.rows, dscratch);
-  AQP_CUDA(cudaGetLastError());
-  int span = 0;
-  AQP_CUDA(cudaMemcpyAsync(&span, dscratch, sizeof(int), cudaMemcpyDeviceToHost, st));
-  AQP_CUDA(cudaMemsetAsync(ctr, 0, (kTileSlots + 1) * sizeof(unsigned), st));
-  AQP_CUDA(cudaStreamSynchronize(st));
-  if (span <= kBandSpan) M.tile_ctr = ctr;
-  return AQP_OK;
-}
-
 __global__ void k_fill_sellp(const int *__restrict__ ptr, const int *__restrict__ idx, const double *__restrict__ val,
                              int rows, const uint8_t *__restrict__ perm, const int64_t *__restrict__ off, int *sidx,
                              double *sval) {
@@ -597,7 +559,6 @@ void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz) {
   s.seg_ticket = (unsigned *)b.take(s.seg_cap * sizeof(unsigned));
   s.sell_off = (int64_t *)b.take(((rows + 255) / 256 * 8 + 2) * sizeof(int64_t));
   s.sell_perm = (uint8_t *)b.take(std::max<int64_t>(rows, 1));
-  s.tile_ctr = (unsigned *)b.take((kTileSlots + 1) * sizeof(unsigned));
 }
 
 // Upload an int64 CSR (device pointers) into int32 storage and plan it.
@@ -1170,7 +1131,6 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
       if (i >= 3 && (d->quad_kind != AQP_QUAD_SPARSE_LOW_RANK || p->r_dense)) continue;
       rc = plan_sell(ctx, *mats[i], stores[i]->sell_off, stores[i]->sell_perm, i == 1, sc, &p->sell_total[i],
                      &p->sell_sorted[i]);
-      if (!rc) rc = plan_tile_order(ctx, *mats[i], stores[i]->tile_ctr, p->bad + 8);
       if (rc) return cleanup(rc);
     }
   }

@@ -306,17 +306,3 @@ def test_rollback_branches_match_reference(cuda, fname):
     # the round counter at every certification point follows the reference's
     assert [r for _, r in trace] == [t[5] for t in g["trace"]]
 
-
-def test_banded_tile_order_is_bitwise_neutral(cuda, monkeypatch):
-    """Banded matrices (C5's A, A', Q at >= 303k rows) run their tiles in
-    per-SM claim order (DevCsr::tile_ctr); partials are stored per tile, so
-    the result is bitwise the blockIdx-order result, run after run."""
-    p = instances.build("c5:5e5:500:0")
-    prm = SolverParams(eps_tol=1e-12, iter_limit=300)
-    runs = []
-    for order in ("1", "1", "0"):
-        monkeypatch.setenv("AQP_TILE_ORDER", order)
-        runs.append(solve(p, prm))
-    for r in runs[1:]:
-        assert (r.outer_iterations, r.inner_iterations) == (runs[0].outer_iterations, runs[0].inner_iterations)
-        assert np.array_equal(r.x, runs[0].x) and np.array_equal(r.y, runs[0].y)
