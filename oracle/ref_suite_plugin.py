@@ -3,8 +3,9 @@ test suite (copied by oracle/build_ref.sh into oracle/_ref/tests, git-ignored)
 against this repo, through the two drop-in boundaries of INTEGRATION.md:
 
 * the kernel registry: this package's ``kernels`` module is registered as the
-  reference backend "cuda" (``anchorqp/_kernels/__init__.py:29``), so every
-  ``kernel_backend``-parametrised test also runs on the B200 kernels;
+  reference backend "cuda" (``anchorqp/_kernels/__init__.py:29``) and selected as
+  the active backend, so every reference function that calls a kernel runs on
+  the B200 kernels, and every ``kernel_backend``-parametrised test also runs them;
 * the solve entry point: ``anchorqp.solve`` / ``anchorqp.engine.solve`` are
   routed to ``paper_2602_23967_b200.solve`` and its result is rebuilt as the
   reference's own ``SolveResult`` / ``ResidualReport`` / ``Certificate``.
@@ -52,6 +53,11 @@ class _CountingBackend:
 
 rkern._BACKENDS["cuda"] = _CountingBackend(b200_kernels)
 _reference_solve = reng.solve
+# the B200 kernels are the ACTIVE backend for the whole suite (the reference's
+# own Python -- pdhg_step, solve_bb, residuals, linalg products -- then runs on
+# them wherever it calls a kernel); AQP_REF_SUITE_BACKEND=cython keeps the
+# reference's default and only routes the kernel_backend-parametrised tests
+rkern.select_backend(os.environ.get("AQP_REF_SUITE_BACKEND", "cuda"))
 
 
 def _to_reference(res):
