@@ -1220,16 +1220,27 @@ __global__ void __launch_bounds__(kFinThreads) fin_ctrl_op(Op op, GridRed g, uns
 // whole virtual warps, same xor trees -- and the warp totals go to CTA 0
 // through distributed shared memory, which adds them in warp order: bitwise
 // the one-block fold, with 8 SMs pulling the partials.
+// The cluster fold is a virtual VT-thread fold: virtual thread v sums
+// partials v, v + VT, ... (batched 4 at a time), then the warp trees and the
+// warp totals in virtual-warp order.  VT = 1024 (8 CTAs x 128) for up to
+// kWideFoldMin partials, else 8192 (8 x 1024): C5's gradient pass leaves
+// 195,313 partials per sum, which 1024 virtual threads summed in dependent
+// chains of 190 (61 us per fold in the device trace; 8192: 19 us), while on
+// C2 (3,906 partials) the wide fold is slower (9 -> 15 us).  For nb <= 1024
+// both widths fold in the same order (the extra virtual warps add exact zeros).
 constexpr int kFoldCtas = 8;
-constexpr int kFoldThreads = kFinThreads / kFoldCtas;
+constexpr int kFoldVT = 1024;
+constexpr int kFoldVTWide = 8192;
+constexpr unsigned kWideFoldMin = 32768;
 
-template <class Op>
-__global__ void __cluster_dims__(kFoldCtas, 1, 1) __launch_bounds__(kFoldThreads)
+template <class Op, int VT>
+__global__ void __cluster_dims__(kFoldCtas, 1, 1) __launch_bounds__(VT / kFoldCtas)
     fin_ctrl_cl(Op op, GridRed g, unsigned nb) {
   namespace cg = cooperative_groups;
   constexpr int NS = Op::NS, NM = Op::NM, NT = NS + NM;
   constexpr int W = (int)(sizeof(Ctrl) / 8);
-  constexpr int NW = kFinThreads / 32;
+  constexpr int kFoldThreads = VT / kFoldCtas;
+  constexpr int NW = VT / 32;
   __shared__ unsigned long long cbuf[W];
   __shared__ double swarp[NW * (NT > 0 ? NT : 1)];
   cg::cluster_group cl = cg::this_cluster();
@@ -1254,12 +1265,12 @@ __global__ void __cluster_dims__(kFoldCtas, 1, 1) __launch_bounds__(kFoldThreads
   a.zero();
   if constexpr (NT > 0) {
     constexpr int U = 4;
-    const unsigned vt = crank * kFoldThreads + threadIdx.x;  // virtual thread of the 1024-thread fold
-    for (unsigned b0 = vt; b0 < nb; b0 += U * kFinThreads) {
+    const unsigned vt = crank * kFoldThreads + threadIdx.x;  // virtual thread of the VT-thread fold
+    for (unsigned b0 = vt; b0 < nb; b0 += U * VT) {
       double t[U][NT];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const unsigned b = b0 + u * kFinThreads;
+        const unsigned b = b0 + u * VT;
 #pragma unroll
         for (int i = 0; i < NT; ++i) t[u][i] = b < nb ? g.partials[(size_t)i * nb + b] : 0.0;
       }
@@ -1457,6 +1468,23 @@ cudaError_t node_elem(cudaGraph_t g, GNode &last, int64_t n, const Op &op, GridR
   return add_node(g, last, (unsigned)elem_grid(n), elem_op<Op>, n, op, gr);
 }
 
+// the cluster fold of `nb` partials, its width chosen by nb (fin_ctrl_cl)
+template <class Op>
+cudaError_t node_fold(cudaGraph_t g, GNode &last, const Op &op, GridRed gr, unsigned nb) {
+  if (nb >= kWideFoldMin)
+    return add_node_cfg(g, last, (unsigned)kFoldCtas, (unsigned)(kFoldVTWide / kFoldCtas), 0u,
+                        fin_ctrl_cl<Op, kFoldVTWide>, op, gr, nb);
+  return add_node_cfg(g, last, (unsigned)kFoldCtas, (unsigned)(kFoldVT / kFoldCtas), 0u, fin_ctrl_cl<Op, kFoldVT>,
+                      op, gr, nb);
+}
+template <class Op>
+void run_fold(cudaStream_t st, const Op &op, GridRed gr, unsigned nb) {
+  if (nb >= kWideFoldMin)
+    fin_ctrl_cl<Op, kFoldVTWide><<<kFoldCtas, kFoldVTWide / kFoldCtas, 0, st>>>(op, gr, nb);
+  else
+    fin_ctrl_cl<Op, kFoldVT><<<kFoldCtas, kFoldVT / kFoldCtas, 0, st>>>(op, gr, nb);
+}
+
 // SPLIT ops: the main launch followed by its one-block fold/finalize
 template <class Op>
 cudaError_t node_spmv_fin(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
@@ -1466,8 +1494,7 @@ cudaError_t node_spmv_fin(cudaGraph_t g, GNode &last, const DevCsr &M, const Op 
                                                 op, gr);
   if (e != cudaSuccess) return e;
 #if AQP_FOLD_CLUSTER
-  return add_node_cfg(g, last, (unsigned)kFoldCtas, (unsigned)kFoldThreads, 0u, fin_ctrl_cl<Op>, op, gr,
-                      (unsigned)M.nitems);
+  return node_fold(g, last, op, gr, (unsigned)M.nitems);
 #else
   return add_node_cfg(g, last, 1u, (unsigned)kFinThreads, 0u, fin_ctrl_op<Op>, op, gr, (unsigned)M.nitems);
 #endif
@@ -1477,8 +1504,7 @@ cudaError_t node_elem_fin(cudaGraph_t g, GNode &last, int64_t n, const Op &op, G
   cudaError_t e = add_node(g, last, (unsigned)elem_grid(n), elem_op<Op>, n, op, gr);
   if (e != cudaSuccess) return e;
 #if AQP_FOLD_CLUSTER
-  return add_node_cfg(g, last, (unsigned)kFoldCtas, (unsigned)kFoldThreads, 0u, fin_ctrl_cl<Op>, op, gr,
-                      (unsigned)elem_grid(n));
+  return node_fold(g, last, op, gr, (unsigned)elem_grid(n));
 #else
   return add_node_cfg(g, last, 1u, (unsigned)kFinThreads, 0u, fin_ctrl_op<Op>, op, gr, (unsigned)elem_grid(n));
 #endif
@@ -1514,7 +1540,7 @@ cudaError_t run_spmv_fin(cudaStream_t st, const DevCsr &M, const Op &op, GridRed
   else
     spmv_op<Op><<<M.nitems, kThreads, M.smem_bytes, st>>>(M, op, gr);
 #if AQP_FOLD_CLUSTER
-  fin_ctrl_cl<Op><<<kFoldCtas, kFoldThreads, 0, st>>>(op, gr, (unsigned)M.nitems);
+  run_fold(st, op, gr, (unsigned)M.nitems);
 #else
   fin_ctrl_op<Op><<<1, kFinThreads, 0, st>>>(op, gr, (unsigned)M.nitems);
 #endif
@@ -1524,7 +1550,7 @@ template <class Op>
 cudaError_t run_elem_fin(cudaStream_t st, int64_t n, const Op &op, GridRed gr) {
   elem_op<Op><<<elem_grid(n), kThreads, 0, st>>>(n, op, gr);
 #if AQP_FOLD_CLUSTER
-  fin_ctrl_cl<Op><<<kFoldCtas, kFoldThreads, 0, st>>>(op, gr, (unsigned)elem_grid(n));
+  run_fold(st, op, gr, (unsigned)elem_grid(n));
 #else
   fin_ctrl_op<Op><<<1, kFinThreads, 0, st>>>(op, gr, (unsigned)elem_grid(n));
 #endif
@@ -2355,7 +2381,7 @@ int aqp_solver_time_kernel(aqp_solver *s, int kernel, int reps, void *flush, siz
         OpGrad<false> o{};
         o.v = v;
 #if AQP_FOLD_CLUSTER
-        fin_ctrl_cl<OpGrad<false>><<<kFoldCtas, kFoldThreads, 0, st>>>(o, gr, (unsigned)p->Q.nitems);
+        run_fold(st, o, gr, (unsigned)p->Q.nitems);
 #else
         fin_ctrl_op<OpGrad<false>><<<1, kFinThreads, 0, st>>>(o, gr, (unsigned)p->Q.nitems);
 #endif
