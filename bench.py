@@ -370,11 +370,12 @@ def run_ours(args, world, rank, local):
     kernels, fixed, per_inner = kernel_table(problem, local, ("bb_gradient", "bb_step", "p1_At_y", "p2_A_xbar",
                                                               "x_post", "bb_fold"))
     top = kernels["bb_gradient"]
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
+    traffic = None  # ncu dram__bytes_{read,write}.sum of the same kernel (scripts/profile_r02.sh)
+    for prof in ("ncu_summary_r02.json", "ncu_summary.json"):
         try:
-            traffic = json.load(open(prof))["kernels"]["c5_bb_gradient"]["dram_bytes_per_launch"]
+            traffic = json.load(open(os.path.join(ROOT, "profiles", prof)))["kernels"]["c5_bb_gradient"][
+                "dram_bytes_per_launch"]
+            break
         except Exception:
             traffic = None
     nnz_q = q_full_nnz(problem)

@@ -87,19 +87,20 @@ def digest(rep):
     return out
 
 
-launch_share()
-names = {"c2_bb_gradient": ["bb_gradient"], "c2_bb_step": ["bb_step"], "c2_bb_fold": ["bb_fold"],
-         "c2_p1": ["c2_p1_At_y"], "c2_p2": ["c2_p2_A_xbar"],
-         "c5_passes": ["c5_bb_gradient", "c5_p1_At_y", "c5_p2_A_xbar"], "c3_dense": ["c3_dense_Rx", "c3_dense_Rtv"]}
-summary = {"tag": tag, "note": "ncu --set full --clock-control none; one launch per kernel; C2 from an eager "
-           "window (scripts/prof_c2.py), C5/C3 stand-alone launches (scripts/prof_kernel.py)", "kernels": {}}
-for rep in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "ncu", "*.ncu-rep"))):
-    base = os.path.basename(rep)[:-8]
-    if base not in names:
-        continue
-    for key, dg in zip(names[base], digest(rep)):
-        summary["kernels"][key] = dg
-with open(os.path.join(OUT, "ncu_summary.json"), "w") as f:
-    json.dump(summary, f, indent=1)
-print(json.dumps({k: (v["kernel"], v["details"].get("Duration"), v["details"].get("DRAM Throughput"))
-                  for k, v in summary["kernels"].items()}, indent=1))
+if __name__ == "__main__":
+    launch_share()
+    names = {"c2_bb_gradient": ["bb_gradient"], "c2_bb_step": ["bb_step"], "c2_bb_fold": ["bb_fold"],
+             "c2_p1": ["c2_p1_At_y"], "c2_p2": ["c2_p2_A_xbar"],
+             "c5_passes": ["c5_bb_gradient", "c5_p1_At_y", "c5_p2_A_xbar"], "c3_dense": ["c3_dense_Rx", "c3_dense_Rtv"]}
+    summary = {"tag": tag, "note": "ncu --set full --clock-control none; one launch per kernel; C2 from an eager "
+               "window (scripts/prof_c2.py), C5/C3 stand-alone launches (scripts/prof_kernel.py)", "kernels": {}}
+    for rep in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "ncu", "*.ncu-rep"))):
+        base = os.path.basename(rep)[:-8]
+        if base not in names:
+            continue
+        for key, dg in zip(names[base], digest(rep)):
+            summary["kernels"][key] = dg
+    with open(os.path.join(OUT, "ncu_summary.json"), "w") as f:
+        json.dump(summary, f, indent=1)
+    print(json.dumps({k: (v["kernel"], v["details"].get("Duration"), v["details"].get("DRAM Throughput"))
+                      for k, v in summary["kernels"].items()}, indent=1))
