@@ -397,6 +397,20 @@ struct __align__(16) PlanItem {
   int kind, seg, nseg, segbase;
 };
 
+// SELL-32 element position of nonzero k of the row at SELL position p:
+// `off` = the slice's offset (sell_off[p / 32]), lane = p % 32.  Pair layout
+// (the non-symmetric A / A' / R / R'): [k0 k1 of lane 0, k0 k1 of lane 1, ...] per
+// pair of steps, even slice widths -- one 128-bit load fetches a lane's two
+// values and one 64-bit load its two column indices (C5-shaped A' / A passes
+// 4-5% faster).  Plain layout (Q): k-major, one entry per lane -- the pair
+// layout made the 4-nonzero rows of the gradient pass 20% slower.
+__host__ __device__ __forceinline__ int64_t sell_pos(int64_t off, int lane, int k, bool pair) {
+  return pair ? off + 64 * (int64_t)(k >> 1) + 2 * lane + (k & 1) : off + 32 * (int64_t)k + lane;
+}
+__host__ __device__ __forceinline__ int64_t sell_width(int longest, bool pair) {  // entries per slice
+  return 32 * (int64_t)(pair ? (longest + 1) & ~1 : longest);
+}
+
 // device CSR with int32 indices plus its work plan
 struct DevCsr {
   int rows = 0, cols = 0;
@@ -416,6 +430,10 @@ struct DevCsr {
   // row r sits at sell_off[r / 32] + 32 k + r % 32, so the warp's k-th loads
   // (one row per lane) are coalesced -- one L1 wavefront for 32 indices
   // instead of ~5 for the strided CSR rows.  Same nonzeros, same order per row.
+  // (non-symmetric matrices: pair layout -- a lane's nonzeros 2j, 2j+1 are
+  // adjacent, so one 128-bit load fetches two values and one 64-bit load two
+  // column indices; the warp still reads contiguous 512 B / 256 B per pair
+  // step; see sell_pos)
   const int64_t *sell_off = nullptr;
   const int *sell_idx = nullptr;
   const double *sell_val = nullptr;

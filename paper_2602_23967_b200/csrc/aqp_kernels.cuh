@@ -185,6 +185,44 @@ __device__ __forceinline__ bool grid_end(RedVals<NS, NM> &v, GridRed g, double *
 #define AQP_SELL_BATCH AQP_GATHER_BATCH
 #endif
 
+// Load the SELL entries k .. k+AQP_SELL_BATCH-1 of one row (lane `lane` of
+// the slice at `off`) into cc / pv; entries past `len` are not used.  PAIR:
+// the pair layout (non-symmetric matrices) -- two 128-bit value loads and two
+// 64-bit index loads per batch of 4.  The layout follows the matrix kind and
+// so the op: every non-symmetric matrix (A, A', R, R') is stored in pairs,
+// the symmetric Q plainly, so PAIR = !Op::SYM is a compile-time choice (a
+// runtime flag cost 2-7% on every pass: code and registers for both paths).
+template <bool PAIR>
+__device__ __forceinline__ void sell_load(const DevCsr &M, int64_t off, int lane, int k, int len,
+                                          int (&cc)[AQP_SELL_BATCH], double (&pv)[AQP_SELL_BATCH]) {
+  static_assert(AQP_SELL_BATCH % 2 == 0, "the pair layout loads whole pairs");
+  if constexpr (PAIR) {
+#pragma unroll
+    for (int h = 0; h < AQP_SELL_BATCH / 2; ++h) {
+      const int kk = k + 2 * h;
+      if (kk < len) {
+        const int64_t q = sell_pos(off, lane, kk, true);
+        const int2 ci = __ldg(reinterpret_cast<const int2 *>(M.sell_idx + q));
+        const double2 vv = __ldg(reinterpret_cast<const double2 *>(M.sell_val + q));
+        cc[2 * h] = ci.x;
+        cc[2 * h + 1] = ci.y;
+        pv[2 * h] = vv.x;
+        pv[2 * h + 1] = vv.y;
+      } else {
+        cc[2 * h] = cc[2 * h + 1] = 0;
+        pv[2 * h] = pv[2 * h + 1] = 0.0;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < AQP_SELL_BATCH; ++u) {
+      const bool in = k + u < len;
+      cc[u] = in ? __ldg(M.sell_idx + sell_pos(off, lane, k + u, false)) : 0;
+      pv[u] = in ? __ldg(M.sell_val + sell_pos(off, lane, k + u, false)) : 0.0;
+    }
+  }
+}
+
 // UNIFORM: the plan is all THREAD items over [256 b, 256 b + 256) (the common
 // case of short-row matrices, e.g. every C2 pass); the instantiation then
 // carries only the thread-per-row path, which needs far fewer registers
@@ -234,23 +272,39 @@ __device__ __forceinline__ void spmv_item(const DevCsr &M, const PlanItem &it, c
       if ((UNIFORM || M.uniform) && M.sell_idx) {
         // SELL-32: the warp's k-th nonzeros are contiguous (coalesced loads)
         const int len = e - b;
-        const int64_t base = __ldg(M.sell_off + (r >> 5)) + (r & 31);
-        for (int k = 0; k < len; k += AQP_SELL_BATCH) {
-          int cc[AQP_SELL_BATCH];
-          double pv[AQP_SELL_BATCH];
+        if constexpr (!Op::SYM) {  // pair layout (A, A', R, R')
+          const int64_t soff = __ldg(M.sell_off + (r >> 5));
+          for (int k = 0; k < len; k += AQP_SELL_BATCH) {
+            int cc[AQP_SELL_BATCH];
+            double pv[AQP_SELL_BATCH];
+            sell_load<true>(M, soff, r & 31, k, len, cc, pv);
 #pragma unroll
-          for (int u = 0; u < AQP_SELL_BATCH; ++u) {
-            const bool in = k + u < len;
-            cc[u] = in ? __ldg(M.sell_idx + base + 32 * (k + u)) : 0;
-            pv[u] = in ? __ldg(M.sell_val + base + 32 * (k + u)) : 0.0;
+            for (int u = 0; u < AQP_SELL_BATCH; ++u)
+              if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);
+#pragma unroll
+            for (int u = 0; u < AQP_SELL_BATCH; ++u)
+              if (k + u < len) up += pv[u];
           }
+        } else {  // plain layout (Q); written out here: this schedule is the
+                  // gradient pass's best (the shared loader cost it 7%)
+          const int64_t base = __ldg(M.sell_off + (r >> 5)) + (r & 31);
+          for (int k = 0; k < len; k += AQP_SELL_BATCH) {
+            int cc[AQP_SELL_BATCH];
+            double pv[AQP_SELL_BATCH];
 #pragma unroll
-          for (int u = 0; u < AQP_SELL_BATCH; ++u)
-            if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);
+            for (int u = 0; u < AQP_SELL_BATCH; ++u) {
+              const bool in = k + u < len;
+              cc[u] = in ? __ldg(M.sell_idx + base + 32 * (k + u)) : 0;
+              pv[u] = in ? __ldg(M.sell_val + base + 32 * (k + u)) : 0.0;
+            }
 #pragma unroll
-          for (int u = 0; u < AQP_SELL_BATCH; ++u) {
-            if (k + u < len) {
-              if (Op::SYM && cc[u] < rg) lo += pv[u]; else up += pv[u];
+            for (int u = 0; u < AQP_SELL_BATCH; ++u)
+              if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);
+#pragma unroll
+            for (int u = 0; u < AQP_SELL_BATCH; ++u) {
+              if (k + u < len) {
+                if (Op::SYM && cc[u] < rg) lo += pv[u]; else up += pv[u];
+              }
             }
           }
         }
@@ -417,16 +471,11 @@ __device__ __forceinline__ void spmv_sellp_block(const DevCsr &M, const Op &o, R
     const int rg = r + M.row_off;
     double lo = 0.0, up = 0.0;
     if (Op::SYM && M.diag) up = __ldg(M.diag + r) * o.gather(rg);
-    const int64_t base = __ldg(M.sell_off + (rn >> 5)) + (rn & 31);
+    const int64_t soff = __ldg(M.sell_off + (rn >> 5));
     for (int k = 0; k < len; k += AQP_SELL_BATCH) {
       int cc[AQP_SELL_BATCH];
       double pv[AQP_SELL_BATCH];
-#pragma unroll
-      for (int u = 0; u < AQP_SELL_BATCH; ++u) {
-        const bool in = k + u < len;
-        cc[u] = in ? __ldg(M.sell_idx + base + 32 * (k + u)) : 0;
-        pv[u] = in ? __ldg(M.sell_val + base + 32 * (k + u)) : 0.0;
-      }
+      sell_load<!Op::SYM>(M, soff, rn & 31, k, len, cc, pv);
 #pragma unroll
       for (int u = 0; u < AQP_SELL_BATCH; ++u)
         if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);

@@ -291,14 +291,15 @@ static int counts_to_ptr(int *counts, int rows, int *ptr_out, void *tmp, size_t 
 // SELL-32 copy of a uniform plan's matrix (DevCsr::sell_*): library-owned
 // device memory, released by free_sell (problem destroy / re-plan).
 __global__ void k_fill_sell(const int *__restrict__ ptr, const int *__restrict__ idx, const double *__restrict__ val,
-                            int rows, const int64_t *__restrict__ off, int *sidx, double *sval) {
+                            int rows, const int64_t *__restrict__ off, int *sidx, double *sval, bool pair) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const int b = ptr[r], e = ptr[r + 1];
-  const int64_t base = off[r >> 5] + (r & 31);
+  const int64_t off0 = off[r >> 5];
+  const int lane = r & 31;
   for (int k = 0; k < e - b; ++k) {
-    sidx[base + 32 * k] = idx[b + k];
-    sval[base + 32 * k] = val[b + k];
+    sidx[sell_pos(off0, lane, k, pair)] = idx[b + k];
+    sval[sell_pos(off0, lane, k, pair)] = val[b + k];
   }
 }
 
@@ -314,12 +315,12 @@ void free_sell(DevCsr &M, cudaStream_t st) {
 
 // 32 * (longest row of each 32-row slice); w[nsl] = 0 so the exclusive scan
 // ends with the total
-__global__ void k_sell_width(const int *__restrict__ ptr, int rows, int64_t nsl, int64_t *__restrict__ w) {
+__global__ void k_sell_width(const int *__restrict__ ptr, int rows, int64_t nsl, int64_t *__restrict__ w, bool pair) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s > nsl) return;
   int mx = 0;
   for (int64_t r = 32 * s; r < 32 * s + 32 && r < rows; ++r) mx = max(mx, ptr[r + 1] - ptr[r]);
-  w[s] = 32 * (int64_t)mx;
+  w[s] = sell_width(mx, pair);
 }
 
 // SELL-P: sort every 256-row block's rows by length, descending and stable
@@ -327,7 +328,7 @@ __global__ void k_sell_width(const int *__restrict__ ptr, int rows, int64_t nsl,
 // 0 and sort last); perm[p] = local row at position p; w[slice] = 32 * the
 // slice's first (= longest) key; *long_nnz += nonzeros of the long rows.
 __global__ void __launch_bounds__(256) k_sellp_sort(const int *__restrict__ ptr, int rows, uint8_t *__restrict__ perm,
-                                                    int64_t *__restrict__ w, unsigned long long *long_nnz) {
+                                                    int64_t *__restrict__ w, unsigned long long *long_nnz, bool pair) {
   using Sort = cub::BlockRadixSort<int, 256, 1, int>;
   __shared__ typename Sort::TempStorage tmp;
   const int r = blockIdx.x * 256 + threadIdx.x;
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(256) k_sellp_sort(const int *__restrict__ ptr,
   Sort(tmp).SortDescending(key, val, 0, 6);
   const int64_t p = (int64_t)blockIdx.x * 256 + threadIdx.x;
   if (p < rows) perm[p] = (uint8_t)val[0];
-  if ((threadIdx.x & 31) == 0) w[p >> 5] = 32 * (int64_t)key[0];
+  if ((threadIdx.x & 31) == 0) w[p >> 5] = sell_width(key[0], pair);
 }
 
 // SELL layout of a non-strict matrix into `off` (+ `perm` for SELL-P):
@@ -351,8 +352,8 @@ __global__ void __launch_bounds__(256) k_sellp_sort(const int *__restrict__ ptr,
 //     the long rows hold <= 5% of the nonzeros (C5 P1: 2.55 -> 2.38 ms; on
 //     C2's short random rows the block barrier made it slower, 34 -> 44 us);
 //   else none (*total = 0).
-static int plan_sell(aqp_ctx *ctx, const DevCsr &M, int64_t *off, uint8_t *perm, bool may_sort, Bump &scratch,
-                     int64_t *total, bool *sorted) {
+static int plan_sell(aqp_ctx *ctx, const DevCsr &M, int64_t *off, uint8_t *perm, bool may_sort, bool pair,
+                     Bump &scratch, int64_t *total, bool *sorted) {
   *total = 0;
   *sorted = false;
   const char *e = getenv("AQP_SELL");
@@ -374,7 +375,7 @@ static int plan_sell(aqp_ctx *ctx, const DevCsr &M, int64_t *off, uint8_t *perm,
   int64_t tot = 0;
   if (M.uniform) {
     AQP_CUDA(cudaMemsetAsync(w, 0, (nw + 1) * sizeof(int64_t), st));
-    k_sell_width<<<(int)((nw + 256) / 256), 256, 0, st>>>(M.ptr, M.rows, (M.rows + 31) / 32, w);
+    k_sell_width<<<(int)((nw + 256) / 256), 256, 0, st>>>(M.ptr, M.rows, (M.rows + 31) / 32, w, pair);
     AQP_CUDA(cudaGetLastError());
     AQP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, w, off, (int)(nw + 1), st));
     AQP_CUDA(cudaMemcpyAsync(&tot, off + nw, sizeof(tot), cudaMemcpyDeviceToHost, st));
@@ -387,7 +388,7 @@ static int plan_sell(aqp_ctx *ctx, const DevCsr &M, int64_t *off, uint8_t *perm,
   if (!perm || pad_p <= 0.0 || !may_sort || (double)M.nnz < 8.0 * (double)M.rows) return AQP_OK;
   AQP_CUDA(cudaMemsetAsync(w, 0, (nw + 1) * sizeof(int64_t), st));
   AQP_CUDA(cudaMemsetAsync(lnnz, 0, sizeof(unsigned long long), st));
-  k_sellp_sort<<<(unsigned)nblk, 256, 0, st>>>(M.ptr, M.rows, perm, w, lnnz);
+  k_sellp_sort<<<(unsigned)nblk, 256, 0, st>>>(M.ptr, M.rows, perm, w, lnnz, pair);
   AQP_CUDA(cudaGetLastError());
   AQP_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, w, off, (int)(nw + 1), st));
   unsigned long long ln = 0;
@@ -404,16 +405,17 @@ static int plan_sell(aqp_ctx *ctx, const DevCsr &M, int64_t *off, uint8_t *perm,
 
 __global__ void k_fill_sellp(const int *__restrict__ ptr, const int *__restrict__ idx, const double *__restrict__ val,
                              int rows, const uint8_t *__restrict__ perm, const int64_t *__restrict__ off, int *sidx,
-                             double *sval) {
+                             double *sval, bool pair) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= rows) return;
   const int64_t r = (p & ~(int64_t)255) + perm[p];
   const int b = ptr[r], e = ptr[r + 1];
   if (e - b > kThreadRowMax) return;  // long rows stay in the CSR
-  const int64_t base = off[p >> 5] + (p & 31);
+  const int64_t off0 = off[p >> 5];
+  const int lane = (int)(p & 31);
   for (int k = 0; k < e - b; ++k) {
-    sidx[base + 32 * k] = idx[b + k];
-    sval[base + 32 * k] = val[b + k];
+    sidx[sell_pos(off0, lane, k, pair)] = idx[b + k];
+    sval[sell_pos(off0, lane, k, pair)] = val[b + k];
   }
 }
 
@@ -1129,8 +1131,9 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
     for (int i = 0; i < 5; ++i) {
       if (i == 2 && d->quad_kind == AQP_QUAD_DIAGONAL) continue;
       if (i >= 3 && (d->quad_kind != AQP_QUAD_SPARSE_LOW_RANK || p->r_dense)) continue;
-      rc = plan_sell(ctx, *mats[i], stores[i]->sell_off, stores[i]->sell_perm, i == 1, sc, &p->sell_total[i],
-                     &p->sell_sorted[i]);
+      // pair layout for the non-symmetric matrices (A, A', R, R'), plain for Q
+      rc = plan_sell(ctx, *mats[i], stores[i]->sell_off, stores[i]->sell_perm, i == 1, i != 2, sc,
+                     &p->sell_total[i], &p->sell_sorted[i]);
       if (rc) return cleanup(rc);
     }
   }
@@ -1186,7 +1189,7 @@ int aqp_problem_attach_sell(aqp_problem *p, void *buf, size_t bytes) {
     at += align256((size_t)tot * 8);
     if (p->sell_sorted[i]) {
       k_fill_sellp<<<(M.rows + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, M.val, M.rows, stores[i]->sell_perm,
-                                                         stores[i]->sell_off, sidx, sval);
+                                                         stores[i]->sell_off, sidx, sval, i != 2);
       // the SELL-P kernel runs one block per 256 rows and sums long rows itself
       M.sell_perm = stores[i]->sell_perm;
       M.uniform = 1;
@@ -1194,7 +1197,7 @@ int aqp_problem_attach_sell(aqp_problem *p, void *buf, size_t bytes) {
       M.smem_bytes = 0;
     } else {
       k_fill_sell<<<(M.rows + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, M.val, M.rows, stores[i]->sell_off, sidx,
-                                                        sval);
+                                                        sval, i != 2);
     }
     AQP_CUDA(cudaGetLastError());
     M.sell_off = stores[i]->sell_off;

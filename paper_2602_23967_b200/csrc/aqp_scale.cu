@@ -57,16 +57,20 @@ __global__ void k_scale_csr(DevCsr M, const double *__restrict__ rs, const doubl
 // the SELL-32 copy of a uniform plan's matrix (DevCsr::sell_*) follows its CSR
 // (thread = SELL position: natural SELL position p is row p; SELL-P position
 // p is row (p & ~255) + sell_perm[p], and long rows are not in the slices)
-__global__ void k_scale_sell(DevCsr M, const double *__restrict__ rs, const double *__restrict__ cs) {
+__global__ void k_scale_sell(DevCsr M, const double *__restrict__ rs, const double *__restrict__ cs, bool pair) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= M.rows || !M.sell_val) return;
   const int r = M.sell_perm ? (p & ~255) + M.sell_perm[p] : p;
   const int len = M.ptr[r + 1] - M.ptr[r];
   if (M.sell_perm && len > kThreadRowMax) return;
-  const int64_t base = M.sell_off[p >> 5] + (p & 31);
+  const int64_t off0 = M.sell_off[p >> 5];
+  const int lane = p & 31;
   double *sval = const_cast<double *>(M.sell_val);
   const double s = rs[r];
-  for (int k = 0; k < len; ++k) sval[base + 32 * k] = sval[base + 32 * k] * s * cs[M.sell_idx[base + 32 * k]];
+  for (int k = 0; k < len; ++k) {
+    const int64_t q = sell_pos(off0, lane, k, pair);
+    sval[q] = sval[q] * s * cs[M.sell_idx[q]];
+  }
 }
 
 __global__ void k_scale_dense(double *__restrict__ R, int k, int64_t n, const double *__restrict__ cs) {
@@ -173,9 +177,9 @@ int aqp_problem_scale(aqp_problem *p, int ruiz_iters, int pock_chambolle, double
   if (n) k_scale_csr<<<grid_of(n), 256, 0, st>>>(p->At, D, E, const_cast<double *>(p->At.val));
   if (sparse_q && n) k_scale_csr<<<grid_of(n), 256, 0, st>>>(p->Q, D, D, const_cast<double *>(p->Q.val));
   if (sparse_q && n && p->Q.diag) k_scale_diag<<<grid_of(n), 256, 0, st>>>(const_cast<double *>(p->Q.diag), D, n);
-  if (m && p->A.sell_val) k_scale_sell<<<grid_of(m), 256, 0, st>>>(p->A, E, D);
-  if (n && p->At.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->At, D, E);
-  if (sparse_q && n && p->Q.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->Q, D, D);
+  if (m && p->A.sell_val) k_scale_sell<<<grid_of(m), 256, 0, st>>>(p->A, E, D, true);
+  if (n && p->At.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->At, D, E, true);
+  if (sparse_q && n && p->Q.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->Q, D, D, false);
   if (lowrank) {
     if (p->r_dense) {
       k_scale_dense<<<grid_of((int64_t)p->R.rows * n), 256, 0, st>>>(const_cast<double *>(p->R.val), p->R.rows, n, D);
@@ -185,8 +189,8 @@ int aqp_problem_scale(aqp_problem *p, int ruiz_iters, int pock_chambolle, double
       k_fill<<<grid_of(std::max<int64_t>(p->R.rows, 1)), 256, 0, st>>>(nx1, std::max<int64_t>(p->R.rows, 1), 1.0);
       k_scale_csr<<<grid_of(p->R.rows), 256, 0, st>>>(p->R, nx1, D, const_cast<double *>(p->R.val));
       k_scale_csr<<<grid_of(n), 256, 0, st>>>(p->Rt, D, nx1, const_cast<double *>(p->Rt.val));
-      if (p->R.sell_val) k_scale_sell<<<grid_of(p->R.rows), 256, 0, st>>>(p->R, nx1, D);
-      if (p->Rt.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->Rt, D, nx1);
+      if (p->R.sell_val) k_scale_sell<<<grid_of(p->R.rows), 256, 0, st>>>(p->R, nx1, D, true);
+      if (p->Rt.sell_val) k_scale_sell<<<grid_of(n), 256, 0, st>>>(p->Rt, D, nx1, true);
     }
   }
   if (n) k_scale_vec<<<grid_of(n), 256, 0, st>>>(p->c, p->qd, p->vlo, p->vhi, D, n);
