@@ -63,6 +63,30 @@ def _split(weights: np.ndarray, parts: int) -> List[int]:
     return cuts
 
 
+def _counts(problem):
+    """Column counts of A and of Q's upper triangle (one bincount each over the
+    nonzeros -- the only O(nnz) host passes of the plan), cached on the
+    problem object: every rank of a process group plans the same problem."""
+    cached = getattr(problem, "_aqp_shard_counts", None)
+    if cached is not None:
+        return cached
+    a = problem.constraint_matrix
+    n = problem.n
+    acol = np.bincount(np.asarray(a.indices), minlength=n) if a.nnz else np.zeros(n, dtype=np.int64)
+    q = problem.quad
+    pq = q if q.kind == "sparse" else (q.p if q.kind == "sparse_low_rank" else None)
+    qcol = None
+    if pq is not None:
+        qi = np.asarray(pq.upper.indices)
+        qcol = np.bincount(qi, minlength=n) if len(qi) else np.zeros(n, dtype=np.int64)
+    out = (acol, qcol)
+    try:
+        object.__setattr__(problem, "_aqp_shard_counts", out)
+    except Exception:
+        pass
+    return out
+
+
 def partition(problem, nranks: int) -> List[Rows]:
     """Contiguous row blocks per rank, balanced by per-iteration bytes.
 
@@ -71,16 +95,13 @@ def partition(problem, nranks: int) -> List[Rows]:
     if not 1 <= nranks <= 8:
         raise ValueError("row shards support 1..8 ranks")
     a = problem.constraint_matrix
-    n, m = problem.n, problem.m
     wy = _Y_ROW_BYTES + _NNZ_BYTES * np.diff(np.asarray(a.indptr)).astype(np.float64)
-    colcnt = np.bincount(np.asarray(a.indices), minlength=n).astype(np.float64)
-    wx = _X_ROW_BYTES + _NNZ_BYTES * colcnt
+    acol, qcol = _counts(problem)
+    wx = _X_ROW_BYTES + _NNZ_BYTES * acol.astype(np.float64)
     q = problem.quad
     if q.kind == "sparse":
-        up = q.upper
-        rc = np.diff(np.asarray(up.indptr)).astype(np.float64)
-        cc = np.bincount(np.asarray(up.indices), minlength=n).astype(np.float64)
-        wx = wx + _NNZ_BYTES * (rc + cc)
+        rc = np.diff(np.asarray(q.upper.indptr)).astype(np.float64)
+        wx = wx + _NNZ_BYTES * (rc + qcol.astype(np.float64))
     cx, cy = _split(wx, nranks), _split(wy, nranks)
     return [(cx[k], cx[k + 1], cy[k], cy[k + 1]) for k in range(nranks)]
 
@@ -146,7 +167,7 @@ def plan(problem, nranks: int, parts: Optional[Sequence[Rows]] = None) -> List[R
     n, m = problem.n, problem.m
     ip, ix = np.asarray(a.indptr), np.asarray(a.indices)
     alo, ahi = _row_extents(ip, ix, n)
-    colcnt = np.bincount(ix, minlength=n) if a.nnz else np.zeros(n, dtype=np.int64)
+    colcnt, qcol = _counts(problem)
     ccum = np.concatenate([[0], np.cumsum(colcnt)])
     q = problem.quad
     pq = q if q.kind == "sparse" else (q.p if q.kind == "sparse_low_rank" else None)
@@ -154,10 +175,11 @@ def plan(problem, nranks: int, parts: Optional[Sequence[Rows]] = None) -> List[R
         up = pq.upper
         qp, qi = np.asarray(up.indptr), np.asarray(up.indices)
         qlo, qhi = _row_extents(qp, qi, n)
-        rows = np.repeat(np.arange(n), np.diff(qp))
-        offd = qi != rows
-        # full row i of Q = upper row i + mirrored off-diagonal upper entries (j, i)
-        fullcnt = np.diff(qp) + np.bincount(qi[offd], minlength=n)
+        # full row i of Q = upper row i + mirrored off-diagonal upper entries (j, i):
+        # column i's upper count minus its diagonal (the first entry of a row
+        # that stores it -- upper rows are sorted)
+        has_diag = (qlo == np.arange(n)).astype(np.int64)
+        fullcnt = np.diff(qp) + qcol - has_diag
         fcum = np.concatenate([[0], np.cumsum(fullcnt)])
     out = []
     for r, (n0, n1, m0, m1) in enumerate(parts):
