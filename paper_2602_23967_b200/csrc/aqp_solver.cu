@@ -1686,7 +1686,9 @@ int build_graph(aqp_solver *s) {
     // while the loop continues (their kernels exit at once otherwise).  A
     // WHILE-node iteration boundary costs ~6.5 us (device trace: fold end ->
     // next step start) against ~1 us for a programmatic edge inside the body.
-    int unroll = 2;
+    // Measured (scripts/c2_unroll.py, c1_time.py): 4 vs 2 -- C2 solve 52.9 ->
+    // 51.7 s, C1 0.137 -> 0.130 s, C5 window unchanged; 8 gains C2 little more.
+    int unroll = 4;
     if (const char *e = getenv("AQP_BB_UNROLL")) unroll = std::max(1, atoi(e));
     if (lowrank) unroll = 1;  // the low-rank passes have no conditional exit
     for (int u = 0; u < unroll; ++u) {
