@@ -175,6 +175,9 @@ struct Combine {
 #ifndef AQP_P2_BLOCKS
 #define AQP_P2_BLOCKS 6
 #endif
+#ifndef AQP_X_BATCH  // grid-stride iterations whose loads the X pass issues together
+#define AQP_X_BATCH 3
+#endif
 
 // ================================================================ iteration ops
 // P1 (BB path): lin = c + A'y ; x0 = clamp(x)
@@ -460,9 +463,10 @@ struct OpXPost {
     cb.init(v);
   }
   __device__ void elem(int64_t i, RedVals<1, 0> &acc) const { elem_in(i, load(i), acc); }
-  // batched (elem_op BATCH): 4 iterations' loads in flight per thread -- C5
-  // 0.60 -> see DESIGN.md; same elements in the same order per thread
-  static constexpr int BATCH = 4;
+  // batched (elem_op BATCH): AQP_X_BATCH iterations' loads in flight per thread,
+  // same elements in the same order per thread (C5 X 0.60 -> 0.43 ms; 3 beats 4 and 2
+  // on C5-shaped and C2 passes, scripts/variants_ab.sh)
+  static constexpr int BATCH = AQP_X_BATCH;
   struct In {
     double p, xk, anc, prev, blk;
   };
