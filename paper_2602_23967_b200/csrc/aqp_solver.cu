@@ -1594,10 +1594,21 @@ int run_lowrank(aqp_solver *s, int src) {
   return AQP_OK;
 }
 
+// grid of the paired BB step: no reduction, so any grid gives the same
+// result; AQP_STEP_BLOCKS_PER_SM caps it (A/B knob: 64 vs the reductions' 8
+// blocks per SM -- C5-shaped step 0.066 -> 0.062 ms, C2 unchanged)
+#ifndef AQP_STEP_BLOCKS_PER_SM
+#define AQP_STEP_BLOCKS_PER_SM 64
+#endif
+inline unsigned step_grid(int64_t n) {
+  const int64_t pairs = std::max<int64_t>(n / 2, 1), b = (pairs + kThreads - 1) / kThreads;
+  return (unsigned)std::min<int64_t>(b, 148 * AQP_STEP_BLOCKS_PER_SM);
+}
+
 // stream launch of the BB step (paired 128-bit kernel when the slice is aligned)
 int run_step(cudaStream_t st, const SV &v, const OpStep &o, GridRed gr) {
   if (v.pair_ok)
-    k_step2<<<elem_grid(std::max<int64_t>(v.nl / 2, 1)), kThreads, 0, st>>>(v.nl, o, gr);
+    k_step2<<<step_grid(v.nl), kThreads, 0, st>>>(v.nl, o, gr);
   else
     elem_op<OpStep><<<elem_grid(v.nl), kThreads, 0, st>>>(v.nl, o, gr);
   AQP_CUDA(cudaGetLastError());
@@ -1700,7 +1711,7 @@ int build_graph(aqp_solver *s) {
       st.v = v;
       st.cond = u > 0;
       if (v.pair_ok)  // 16-byte aligned slices: the paired (128-bit) step
-        AQP_CUDA(add_node(ib, il, (unsigned)elem_grid(std::max<int64_t>(v.nl / 2, 1)), k_step2, v.nl, st, gr));
+        AQP_CUDA(add_node(ib, il, step_grid(v.nl), k_step2, v.nl, st, gr));
       else
         AQP_CUDA(node_elem(ib, il, v.nl, st, gr));
       if (s->shard) AQP_CUDA(node_barrier(ib, il, gr));
