@@ -650,11 +650,15 @@ static __global__ void k_comm_barrier(GridRed g) {
 }
 
 // grid of an elementwise pass: a pure function of n (so reductions are
-// reproducible), at most 8 resident 256-thread blocks on each of 148 SMs
+// reproducible), at most AQP_ELEM_BLOCKS_PER_SM 256-thread blocks per SM
+#ifndef AQP_ELEM_BLOCKS_PER_SM
+#define AQP_ELEM_BLOCKS_PER_SM 8
+#endif
+constexpr int kElemGridMax = 148 * AQP_ELEM_BLOCKS_PER_SM;
 __host__ __device__ inline int elem_grid(int64_t n) {
   int64_t b = (n + kThreads - 1) / kThreads;
   if (b < 1) b = 1;
-  if (b > 148 * 8) b = 148 * 8;
+  if (b > kElemGridMax) b = kElemGridMax;
   return (int)b;
 }
 

@@ -1406,7 +1406,7 @@ void layout_solver(Bump &b, aqp_problem *p, SV &v, Ctrl **ctrl, GridRed &gr) {
   // rank: the peer-visible exchange region.  Partials below are sized by this
   // rank's plan.
   gr.comm.cb = (CommBlock *)b.take(sizeof(CommBlock));
-  int64_t maxg = 148 * 8;
+  int64_t maxg = kElemGridMax;
   for (const DevCsr *M : {&p->A, &p->At, &p->Q, &p->R, &p->Rt}) maxg = std::max<int64_t>(maxg, M->nitems);
   gr.partials = (double *)b.take(maxg * kMaxRed * 8);
   gr.ticket = (unsigned *)b.take(64);  // [0] grid_end ticket
