@@ -211,3 +211,61 @@ def test_banded_storage_shrinks_with_ranks():
             assert (me.ywin[1] - me.ywin[0]) <= p.m / P + 2 * 600
             assert me.a_local_nnz + me.at_local_nnz + me.q_local_nnz <= 1.1 * (
                 2 * p.constraint_matrix.nnz + 2 * p.quad.upper.nnz) / P
+
+
+def _setup_worker(rank, world, port, q):
+    """engine._setup_info over a gloo DistGroup with per-rank device structs
+    faked: flags or-ed, first inverted index min-ed over the ranks that have
+    one, maxima max-ed, R's row sums computed on the host for a low-rank Q."""
+    import torch.distributed as dist
+
+    from paper_2602_23967_b200 import _native as nat
+    from paper_2602_23967_b200.engine import _setup_info
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = shard.DistGroup()
+
+        class FakeDev:
+            def setup_info(self):
+                info = nat.SetupInfo()
+                info.var_first_inverted = -1 if rank == 0 else 7
+                info.con_first_inverted = 3 + rank
+                info.q_nonfinite = rank
+                info.con_scale, info.cost_inf = (2.0, 9.0) if rank == 0 else (3.5, 1.0)
+                info.q_bound, info.r_one, info.diag_bound = 1.0 + rank, 4.0 - rank, 0.5 * rank
+                info.r_inf_done = 0
+                return info
+
+        p = instances.build("rqp:300:150:low_rank:0.05:3")
+        info = _setup_info(FakeDev(), p, g)
+        q.put((rank, info.var_first_inverted, info.con_first_inverted, info.q_nonfinite, info.con_scale,
+               info.cost_inf, info.q_bound, info.r_one, info.diag_bound, info.r_inf,
+               float(p.quad.r.row_abs_sums().max(initial=0.0))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_setup_info_combine_gloo_world2():
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_setup_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for pr in procs:
+        pr.join(60)
+        assert pr.exitcode == 0
+    for r in res:
+        _, vinv, cinv, qbad, cscale, cinf, qb, r1, db, rinf, rinf_host = r
+        assert (vinv, cinv, qbad) == (7, 3, 1)
+        assert (cscale, cinf, qb, r1, db) == (3.5, 9.0, 2.0, 4.0, 0.5)
+        assert rinf == rinf_host
