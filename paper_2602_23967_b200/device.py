@@ -79,9 +79,8 @@ def _full_rows(r) -> bool:
         return False
     if not np.array_equal(np.asarray(r.indptr), np.arange(r.rows + 1, dtype=np.int64) * n):
         return False
-    ar = np.arange(n)
-    idx = np.asarray(r.indices)
-    return all(np.array_equal(idx[i * n:(i + 1) * n], ar) for i in range(r.rows))
+    idx = np.asarray(r.indices).reshape(r.rows, n)
+    return bool((idx == np.arange(n, dtype=idx.dtype)).all())
 
 
 class DeviceProblem:
