@@ -57,6 +57,8 @@ struct Ctrl {
   int64_t window_len;
   int pw_stop;
   int bb_cont;     // mirror of the BB WHILE condition (eager mode reads it)
+  int pw_src, pad1;  // power iteration: v = xbb[pw_src] / pw_nrm (OpPwA)
+  double pw_nrm;
   double red[R_COUNT];
 };
 
@@ -1095,6 +1097,7 @@ struct OpPush {
       case 4: p = v.dx[0]; break;
       case 5: p = v.dx[1]; break;
       case 6: p = pick3(v.xbb, 1); break;
+      case 8: p = pick3(v.xbb, 2); break;
       default: p = v.tm; break;
     }
   }
@@ -1105,7 +1108,7 @@ struct OpPush {
   __device__ void finalize(const RedVals<0, 0> &) const {}
 };
 // gathered (windowed) buffers only: a push stores this rank's slice into the peers' windows
-enum PushBuf : int { PB_Y = 0, PB_XEVAL, PB_DY0, PB_DY1, PB_DX0, PB_DX1, PB_PW, PB_TM };
+enum PushBuf : int { PB_Y = 0, PB_XEVAL, PB_DY0, PB_DY1, PB_DX0, PB_DX1, PB_PW, PB_TM, PB_PW2 };
 
 // ---------------------------------------------------------------- scaled solves
 // Certification of a scaled solve (aqp_problem_scale) on the ORIGINAL
@@ -1148,30 +1151,63 @@ struct OpPwNorm {  // sum of squares of xbb[idx] -> red[slot]
   __device__ void finalize(const RedVals<1, 0> &t) const { v.ctrl->red[slot] = t.s[0]; }
 };
 
-struct OpPwScale {  // xbb[dst] = xbb[src] / sqrt(red[slot]); stop when the norm is 0
-  static constexpr int NS = 0, NM = 0;
-  static constexpr bool FINAL = false;
+// The power iteration keeps v implicit: v = xbb[pw_src] / pw_nrm, divided at
+// the gather of the A pass -- the reference's `v = w / nw` (linalg.py:302-308)
+// is the same IEEE quotient, so no pass stores v.  w alternates between xbb[1]
+// and xbb[2] (the start vector stays in xbb[0]), so a stopping iteration
+// (`nw == 0`) leaves the last v intact for the final |A v|.
+template <bool RED>
+struct OpPwA {  // tm = A v  (|A v|^2 -> red[slot] when RED)
+  static constexpr int NS = RED ? 1 : 0, NM = 0;
+  static constexpr bool SYM = false, FINAL = RED;
   SV v;
-  int src, dst, slot;
-  double nrm;
+  int slot;
   const double *x;
-  double *o;
-  __device__ bool skip() const { return v.ctrl->pw_stop != 0 || v.ctrl->red[slot] == 0.0; }
+  double nrm;
+  __device__ bool skip() const { return v.ctrl->pw_stop != 0; }
   __device__ void prepare() {
-    nrm = sqrt(v.ctrl->red[slot]);
-    x = pick3(v.xbb, src);
-    o = pick3(v.xbb, dst);
+    const Ctrl *ct = v.ctrl;
+    x = pick3(v.xbb, ct->pw_src) - v.xoff;
+    nrm = ct->pw_nrm;
   }
-  __device__ void elem(int64_t i, RedVals<0, 0> &) const { o[i] = x[i] / nrm; }
-  static constexpr int BATCH = 4;  // elem_op: 4 loads in flight per thread
-  using In = double;
-  __device__ double load(int64_t i) const { return x[i]; }
-  __device__ void elem_in(int64_t i, double xi, RedVals<0, 0> &) const { o[i] = xi / nrm; }
-  __device__ void finalize(const RedVals<0, 0> &) const {}
+  __device__ double gather(int c) const { return gld(x + c) / nrm; }
+  __device__ void row(int r, double s, RedVals<NS, 0> &acc) const {
+    v.tm[r] = s;
+    if constexpr (RED) acc.s[0] += s * s;
+  }
+  __device__ void finalize(const RedVals<NS, 0> &t) const {
+    if constexpr (RED) v.ctrl->red[slot] = t.s[0];
+  }
 };
 
-__global__ void k_pw_check(Ctrl *ct, int slot) {
-  if (ct->red[slot] == 0.0) ct->pw_stop = 1;  // linalg.py:309 `if nw == 0.0: break`
+struct OpPwAt {  // w = A' tm -> xbb[dst], |w|^2; the fold sets the next v (or stops)
+  static constexpr int NS = 1, NM = 0;
+  static constexpr bool SYM = false, FINAL = true, SPLIT = true;
+  SV v;
+  int dst;
+  double *w;
+  __device__ bool skip() const { return v.ctrl->pw_stop != 0; }
+  __device__ void prepare() { w = pick3(v.xbb, dst); }
+  __device__ double gather(int c) const { return gld(v.tm - v.yoff + c); }
+  __device__ void row(int r, double s, RedVals<1, 0> &acc) const {
+    w[r] = s;
+    acc.s[0] += s * s;
+  }
+  __device__ void finalize(const RedVals<1, 0> &t) const {
+    Ctrl *ct = v.ctrl;
+    ct->red[R_PW + 2] = t.s[0];
+    if (t.s[0] == 0.0) {
+      ct->pw_stop = 1;  // linalg.py:307 `if nw == 0.0: break`
+    } else {
+      ct->pw_src = dst;
+      ct->pw_nrm = sqrt(t.s[0]);  // np.linalg.norm(w)
+    }
+  }
+};
+
+__global__ void k_pw_start(Ctrl *ct, int slot) {  // v = xbb[0] / |xbb[0]|
+  ct->pw_src = 0;
+  ct->pw_nrm = sqrt(ct->red[slot]);
 }
 
 // Fold + finalize for the solver's SPLIT ops.  The finalize code (BB step
@@ -2314,29 +2350,25 @@ int aqp_solver_estimate_norm(aqp_solver *s, const double *host_v0, int iters, do
   }
   // nv = |v|; u = v / nv; |A u| > 0 ?
   { OpPwNorm o{}; o.v = v; o.idx = 0; o.slot = R_PW; AQP_CUDA(run_elem(st, n, o, gr)); }
-  { OpPwScale o{}; o.v = v; o.src = 0; o.dst = 1; o.slot = R_PW; AQP_CUDA(run_elem(st, n, o, gr)); }
-  AQP_TRY(push_buf(s, PB_PW));
-  { OpStoreT<false> a{}; a.v = v; a.src = 2; a.dst = 2; a.red = R_PW + 1; AQP_CUDA(run_spmv(st, p->A, a, gr)); }
+  k_pw_start<<<1, 1, 0, st>>>(s->d_ctrl, R_PW);
+  AQP_CUDA(cudaGetLastError());
+  { OpPwA<true> a{}; a.v = v; a.slot = R_PW + 1; AQP_CUDA(run_spmv(st, p->A, a, gr)); }
   AQP_TRY(pull_ctrl(s));
   if (!(s->h.red[R_PW] > 0.0) || !(s->h.red[R_PW + 1] > 0.0)) {
     *annihilated = 1;
     return AQP_OK;
   }
   for (int it = 0; it < iters; ++it) {
-    OpStoreT<false> a{}; a.v = v; a.src = 2; a.dst = 2; a.red = -1;           // t = A v
+    OpPwA<false> a{}; a.v = v;                                   // t = A v
     AQP_CUDA(run_spmv(st, p->A, a, gr));
     AQP_TRY(push_buf(s, PB_TM));
-    OpStoreT<false> b{}; b.v = v; b.src = 3; b.dst = 3; b.red = R_PW + 2;     // w = A't, |w|^2
-    AQP_CUDA(run_spmv(st, p->At, b, gr));
-    k_pw_check<<<1, 1, 0, st>>>(s->d_ctrl, R_PW + 2);
-    AQP_CUDA(cudaGetLastError());
-    OpPwScale c{}; c.v = v; c.src = 2; c.dst = 1; c.slot = R_PW + 2;          // v = w / |w|
-    AQP_CUDA(run_elem(st, n, c, gr));
-    AQP_TRY(push_buf(s, PB_PW));
+    OpPwAt b{}; b.v = v; b.dst = 1 + (it & 1);                   // w = A't, |w|, next v
+    AQP_CUDA(run_spmv_fin(st, p->At, b, gr));
+    AQP_TRY(push_buf(s, b.dst == 1 ? PB_PW : PB_PW2));
   }
   // final |A v| (the stop flag must not suppress it)
   AQP_TRY(poke(s, &Ctrl::pw_stop, 0));
-  { OpStoreT<false> a{}; a.v = v; a.src = 2; a.dst = 2; a.red = R_PW + 3; AQP_CUDA(run_spmv(st, p->A, a, gr)); }
+  { OpPwA<true> a{}; a.v = v; a.slot = R_PW + 3; AQP_CUDA(run_spmv(st, p->A, a, gr)); }
   AQP_TRY(pull_ctrl(s));
   *out = sqrt(s->h.red[R_PW + 3]);
   return AQP_OK;
