@@ -21,7 +21,8 @@ with eps_tol = 1e-8 and the reference's default parameters.
   SURVEY.md §0), max-over-ranks device time.
 * ``e2e`` = the same metric over the WHOLE ``solve`` call (iter_limit = W+K)
   from host buffers: problem upload (H2D), A'/Q build, norm estimate, the W+K
-  iterations, the final check and the read-back of x, y (D2H).
+  iterations, the final check and the read-back of x, y (D2H); the timed call
+  follows one untimed warm-up call of the same solve (steady state).
 * ``roofline``: the dominant kernel of a C5 outer iteration (the BB gradient
   pass: Q SpMV + gradient epilogue + 7 reductions, run 1 + t times per outer
   iteration) timed stand-alone; algorithmic bytes per launch from SURVEY.md
@@ -337,6 +338,12 @@ def run_ours(args, world, rank, local):
     from paper_2602_23967_b200.device import DeviceContext
 
     DeviceContext.get(local)
+    # one untimed warm-up call of the same solve (the first call of a process
+    # also pays the device allocator's first mappings of ~15 GB and the first
+    # touch of the staging path: 1.1 s of upload instead of 0.3 s, AQP_PHASES);
+    # the timed call below is the steady state of a serving process
+    aq.solve(problem, aq.SolverParams(eps_tol=EPS, iter_limit=W + K), device=local, group=group)
+    gc.collect()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -398,7 +405,8 @@ def run_ours(args, world, rank, local):
                 "scope": f"one e2e step = one whole solve call from host (numpy) arrays with iter_limit {W + K}: "
                          f"staged H2D of the problem, device validation and A'/Q/SELL build, norm estimate, all "
                          f"{W + K} outer iterations, final check, D2H of x, y and the dual slack; value = its BB "
-                         f"iterations / its wall time (libaqp context created before the timer)"},
+                         f"iterations / its wall time (libaqp context created and one untimed warm-up call of the same solve "
+                         f"before the timer)"},
         "roofline": {"bound": "hbm", "achieved": top["gbs"], "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": top["gbs"] / peak, "traffic": traffic,
                      "kernel": "C5 bb_gradient (Q SpMV + gradient epilogue + 7 sums)",

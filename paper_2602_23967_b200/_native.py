@@ -58,6 +58,7 @@ class ProblemInfo(C.Structure):
         ("a_items", C.c_int64), ("at_items", C.c_int64), ("q_items", C.c_int64),
         ("quad_kind", C.c_int32), ("r_dense", C.c_int32),
         ("persistent_bytes", C.c_size_t),
+        ("ring_mask", C.c_int32),
     ]
 
 

@@ -43,6 +43,9 @@ constexpr int kTileNnz = 2048;         // nonzeros staged per SpMV row-block (16
 constexpr int kSegNnz = 8192;          // nonzeros per block for a split long row
 constexpr int kThreadRowMax = 48;      // longest row handled one-thread-per-row
 constexpr int kMaxRed = 16;            // max reduction slots of one kernel
+constexpr int kRingRT = 1024;          // ring path: rows per group (kRingRT / kThreads tiles)
+constexpr int kRingSub = kRingRT / kThreads;
+constexpr int kRingS = 16384;          // ring path: cached columns of the gathered vector (128 KB)
 
 // ---------------------------------------------------------------- scalar helpers
 // Reference semantics: _clip in _core.pyx:21-26 (lo first, then hi; NaN passes through)
@@ -452,6 +455,13 @@ struct DevCsr {
   // diagonal is the first j >= i entry, so the order is unchanged -- and the
   // CSR loop is one nonzero (often one gather batch) shorter.
   const double *diag = nullptr;
+  // banded ring path (spmv_ring_op, unsharded SELL / SELL-P matrices whose
+  // nonzeros stay within a moving column window): per group of kRingRT rows
+  // the column window [x, y] its rows gather, made monotone (x: suffix
+  // minimum, y: prefix maximum); null when the band does not fit the ring
+  const int2 *win = nullptr;
+  int win_groups = 0;
+  int win_grid = 0;  // persistent grid: one 1024-thread CTA per SM
 };
 
 }  // namespace aqp

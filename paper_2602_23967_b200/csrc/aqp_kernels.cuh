@@ -567,6 +567,280 @@ __global__ void __launch_bounds__(kThreads, UniformBlocksOf<Op>::value) spmv_sel
   }
 }
 
+// ---------------------------------------------------------------- banded ring path
+// SpMV passes over banded matrices (C5's A, A', Q: every row's columns lie
+// within +-w of the row) gather from a ring of the source vector held in
+// shared memory instead of from L2.  One 1024-thread CTA per SM walks a
+// contiguous strip of row groups (kRingRT rows = kRingSub tiles of 256); per
+// group it adds the ~kRingRT columns the band newly reaches (DevCsr::win, read
+// from HBM once per strip) while the group's rows gather their products from
+// the ring -- random 8-byte L2 sector reads become shared-memory loads, and the
+// matrix stream has the memory system to itself.  Each 256-thread sub-block
+// runs one tile exactly as spmv_op / spmv_sellp_op would (same row -> thread
+// map, same per-row summation order, same xor-shuffle + warp-order reduction,
+// partials stored at the tile's block slot), so results and reductions are
+// bitwise those of the non-ring kernels.  Measured on a C5-shaped pass with a
+// light epilogue (scripts/native/band_bench.cu): 1.33 -> 1.05 ms.
+
+// named barrier of sub-block `sub` (ids 1..kRingSub; 0 is __syncthreads)
+__device__ __forceinline__ void sub_sync(int sub) {
+  asm volatile("bar.sync %0, %1;" ::"r"(sub + 1), "r"(kThreads) : "memory");
+}
+__device__ __forceinline__ int sub_sync_count(int sub, bool pred) {
+  int n;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.popc.u32 %0, %2, %3, p;\n\t}"
+      : "=r"(n)
+      : "r"((unsigned)pred), "r"(sub + 1), "r"(kThreads)
+      : "memory");
+  return n;
+}
+
+// block_reduce over one 256-thread sub-block (same tree, same warp order)
+template <int NS, int NM>
+__device__ __forceinline__ void sub_reduce(RedVals<NS, NM> &v, double *smem, int sub) {
+  constexpr int NT = NS + NM;
+  if constexpr (NT == 0) return;
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) & (kWarps - 1);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) v.s[i] += __shfl_xor_sync(0xffffffffu, v.s[i], off);
+#pragma unroll
+    for (int i = 0; i < NM; ++i) v.m[i] = nanmax(v.m[i], __shfl_xor_sync(0xffffffffu, v.m[i], off));
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) smem[warp * NT + i] = v.s[i];
+#pragma unroll
+    for (int i = 0; i < NM; ++i) smem[warp * NT + NS + i] = v.m[i];
+  }
+  sub_sync(sub);
+  if ((threadIdx.x & (kThreads - 1)) == 0) {
+#pragma unroll
+    for (int i = 0; i < NS; ++i) v.s[i] = smem[i];
+#pragma unroll
+    for (int i = 0; i < NM; ++i) v.m[i] = smem[NS + i];
+    for (int w = 1; w < kWarps; ++w) {
+#pragma unroll
+      for (int i = 0; i < NS; ++i) v.s[i] += smem[w * NT + i];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) v.m[i] = nanmax(v.m[i], smem[w * NT + NS + i]);
+    }
+  }
+  sub_sync(sub);
+}
+
+// the op with its gather served from the ring
+template <class Op>
+struct RingOp : Op {
+  const double *ring_;
+  __device__ __forceinline__ double gather(int c) const { return ring_[c & (kRingS - 1)]; }
+};
+
+// row r of a natural SELL-32 matrix (spmv_item's THREAD path on SELL storage)
+template <class O>
+__device__ __forceinline__ void ring_sell_row(const DevCsr &M, const O &o, int r, RedVals<O::NS, O::NM> &acc) {
+  if (r >= M.rows) return;
+  using RowIn = typename RowInOf<O>::type;
+  RowIn rin{};
+  if constexpr (RowInOf<O>::value && !RowInLateOf<O>::value) rin = o.load_row(r);
+  const int b = __ldg(M.ptr + r), e = __ldg(M.ptr + r + 1);
+  const int rg = r + M.row_off;
+  double lo = 0.0, up = 0.0;
+  if (O::SYM && M.diag) up = __ldg(M.diag + r) * o.gather(rg);
+  const int len = e - b;
+  if constexpr (!O::SYM) {
+    const int64_t soff = __ldg(M.sell_off + (r >> 5));
+    for (int k = 0; k < len; k += AQP_SELL_BATCH) {
+      int cc[AQP_SELL_BATCH];
+      double pv[AQP_SELL_BATCH];
+      sell_load<true>(M, soff, r & 31, k, len, cc, pv);
+#pragma unroll
+      for (int u = 0; u < AQP_SELL_BATCH; ++u)
+        if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);
+#pragma unroll
+      for (int u = 0; u < AQP_SELL_BATCH; ++u)
+        if (k + u < len) up += pv[u];
+    }
+  } else {
+    const int64_t base = __ldg(M.sell_off + (r >> 5)) + (r & 31);
+    for (int k = 0; k < len; k += AQP_SELL_BATCH) {
+      int cc[AQP_SELL_BATCH];
+      double pv[AQP_SELL_BATCH];
+#pragma unroll
+      for (int u = 0; u < AQP_SELL_BATCH; ++u) {
+        const bool in = k + u < len;
+        cc[u] = in ? __ldg(M.sell_idx + base + 32 * (k + u)) : 0;
+        pv[u] = in ? __ldg(M.sell_val + base + 32 * (k + u)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < AQP_SELL_BATCH; ++u)
+        if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);
+#pragma unroll
+      for (int u = 0; u < AQP_SELL_BATCH; ++u) {
+        if (k + u < len) {
+          if (O::SYM && cc[u] < rg) lo += pv[u]; else up += pv[u];
+        }
+      }
+    }
+  }
+  const double val = O::SYM ? lo + up : up;
+  if constexpr (RowInOf<O>::value && RowInLateOf<O>::value) rin = o.load_row(r);
+  if constexpr (RowInOf<O>::value) o.row_in(r, val, rin, acc); else o.row(r, val, acc);
+}
+
+// tile `tile` of a SELL-P matrix on sub-block `sub` (spmv_sellp_block with
+// named barriers and the sub-block's shared arrays)
+template <class O>
+__device__ __forceinline__ void ring_sellp_tile(const DevCsr &M, const O &o, int tile, int sub,
+                                                RedVals<O::NS, O::NM> &acc, double *sred, double *ssum, int *lrow,
+                                                int *nlr) {
+  const int blk = tile * kThreads, t = threadIdx.x & (kThreads - 1);
+  const int rn = blk + t;
+  using RowIn = typename RowInOf<O>::type;
+  RowIn rin{};
+  const bool has = rn < M.rows;
+  if constexpr (RowInOf<O>::value && !RowInLateOf<O>::value)
+    if (has) rin = o.load_row(rn);
+  const int r = has ? blk + (int)__ldg(M.sell_perm + rn) : blk;
+  int b = 0, e = 0;
+  if (has) {
+    b = __ldg(M.ptr + r);
+    e = __ldg(M.ptr + r + 1);
+  }
+  const int len = e - b;
+  const bool lng = has && len > kThreadRowMax;
+  if (t == 0) *nlr = 0;
+  if (has && !lng) {
+    const int rg = r + M.row_off;
+    double lo = 0.0, up = 0.0;
+    if (O::SYM && M.diag) up = __ldg(M.diag + r) * o.gather(rg);
+    const int64_t soff = __ldg(M.sell_off + (rn >> 5));
+    for (int k = 0; k < len; k += AQP_SELL_BATCH) {
+      int cc[AQP_SELL_BATCH];
+      double pv[AQP_SELL_BATCH];
+      sell_load<!O::SYM>(M, soff, rn & 31, k, len, cc, pv);
+#pragma unroll
+      for (int u = 0; u < AQP_SELL_BATCH; ++u)
+        if (k + u < len) pv[u] = pv[u] * o.gather(cc[u]);
+#pragma unroll
+      for (int u = 0; u < AQP_SELL_BATCH; ++u) {
+        if (k + u < len) {
+          if (O::SYM && cc[u] < rg) lo += pv[u]; else up += pv[u];
+        }
+      }
+    }
+    ssum[r - blk] = O::SYM ? lo + up : up;
+  }
+  if (sub_sync_count(sub, lng)) {
+    if (lng) lrow[atomicAdd(nlr, 1)] = r;
+    sub_sync(sub);
+    const int nl = *nlr;
+    for (int i = 0; i < nl; ++i) {
+      const int rr = lrow[i], rg = rr + M.row_off;
+      RedVals<2, 0> lu;
+      lu.zero();
+      if (O::SYM && M.diag && t == 0) lu.s[1] = __ldg(M.diag + rr) * o.gather(rg);
+      for (int k = __ldg(M.ptr + rr) + t, ke = __ldg(M.ptr + rr + 1); k < ke; k += kThreads) {
+        const int c = __ldg(M.idx + k);
+        const double pv = __ldg(M.val + k) * o.gather(c);
+        if (O::SYM && c < rg) lu.s[0] += pv; else lu.s[1] += pv;
+      }
+      sub_reduce<2, 0>(lu, sred, sub);
+      if (t == 0) ssum[rr - blk] = O::SYM ? lu.s[0] + lu.s[1] : lu.s[1];
+      sub_sync(sub);
+    }
+  }
+  sub_sync(sub);
+  if (has) {
+    const double val = ssum[t];
+    if constexpr (RowInOf<O>::value && RowInLateOf<O>::value) rin = o.load_row(rn);
+    if constexpr (RowInOf<O>::value) o.row_in(rn, val, rin, acc); else o.row(rn, val, acc);
+  }
+}
+
+// Op::RING = false keeps an op on the tile kernels.  Measured on C5 (bench
+// kernel table, same box): the A x̄ pass P2 1.998 -> 1.863 ms and the power
+// iteration gain; the BB gradient (Q's +-1000 band already hits L1/L2, seven
+// epilogue streams) 1.17 -> 1.75 ms and A'y (P1, SELL-P with its per-tile
+// hand-off barriers, five epilogue streams) 2.29 -> 2.43 ms lose: with one
+// 1024-thread CTA per SM and a barrier per group the epilogue loads of a heavy
+// op are exposed, where 48 independent warps of the tile kernel hide them.
+template <class Op, class = void>
+struct RingOf {
+  static constexpr bool value = true;
+};
+template <class Op>
+struct RingOf<Op, std::void_t<decltype(Op::RING)>> {
+  static constexpr bool value = Op::RING;
+};
+// ops the ring kernel serves: no reduction, or split reductions (partials
+// only -- the last-block ticket of cold ops stays with spmv_op)
+template <class Op>
+constexpr bool kRingable = (!Op::FINAL || SplitOf<Op>::value) && RingOf<Op>::value;
+
+template <class Op, bool SELLP>
+__global__ void __launch_bounds__(kRingRT, 1) spmv_ring_op(DevCsr M, Op op, GridRed g) {
+  constexpr int NS = Op::NS, NM = Op::NM;
+  extern __shared__ double ring[];
+  __shared__ double sred[kRingSub][kWarps * kMaxRed];
+  __shared__ double ssum[SELLP ? kRingRT : 1];
+  __shared__ int lrow[SELLP ? kRingRT : 1];
+  __shared__ int nlr[kRingSub];
+  pdl_wait();
+  trace_mark(g, 0);
+  if (op.skip()) return;
+  RingOp<Op> o;
+  static_cast<Op &>(o) = op;
+  o.prepare();
+  o.ring_ = ring;
+  const Op &src = o;  // the vector the ring caches, through the op's own gather
+  const int t = threadIdx.x, sub = t / kThreads;
+  const int ng = M.win_groups;
+  const int g0 = (int)((int64_t)blockIdx.x * ng / gridDim.x);
+  const int g1 = (int)((int64_t)(blockIdx.x + 1) * ng / gridDim.x);
+  if (g0 < g1) {
+    const int2 w0 = M.win[g0];
+    for (int c = w0.x + t; c <= w0.y; c += kRingRT) ring[c & (kRingS - 1)] = src.gather(c);
+    int have = w0.y;
+    __syncthreads();
+    const unsigned nb = (unsigned)M.nitems;
+    for (int gi = g0; gi < g1; ++gi) {
+      // the next group's new columns: loaded now, stored after this group's
+      // rows (the plan guarantees win[g+1].y - win[g].x < kRingS, so they
+      // never overwrite a column this group still reads)
+      const int nh = gi + 1 < g1 ? M.win[gi + 1].y : have;
+      const int c0 = have + 1 + t, c1 = c0 + kRingRT;
+      const double p0 = c0 <= nh ? src.gather(c0) : 0.0;
+      const double p1 = c1 <= nh ? src.gather(c1) : 0.0;
+      const int tile = gi * kRingSub + sub;
+      if (tile < M.nitems) {
+        RedVals<NS, NM> acc;
+        acc.zero();
+        if constexpr (SELLP)
+          ring_sellp_tile(M, o, tile, sub, acc, sred[sub], ssum + sub * kThreads, lrow + sub * kThreads, nlr + sub);
+        else
+          ring_sell_row(M, o, tile * kThreads + (t & (kThreads - 1)), acc);
+        if constexpr (Op::FINAL && NS + NM > 0) {
+          sub_reduce<NS, NM>(acc, sred[sub], sub);
+          if ((t & (kThreads - 1)) == 0) {
+#pragma unroll
+            for (int i = 0; i < NS; ++i) g.partials[(size_t)i * nb + tile] = acc.s[i];
+#pragma unroll
+            for (int i = 0; i < NM; ++i) g.partials[(size_t)(NS + i) * nb + tile] = acc.m[i];
+          }
+        }
+      }
+      if (c0 <= nh) ring[c0 & (kRingS - 1)] = p0;
+      if (c1 <= nh) ring[c1 & (kRingS - 1)] = p1;
+      have = nh;
+      __syncthreads();
+    }
+  }
+  pdl_trigger();
+}
+
 // Op::BATCH (optional, with `struct In; In load(i) const; void elem_in(i,
 // const In&, RedVals&) const`): the loads of BATCH grid-stride iterations are
 // issued before any of their stores (the compiler cannot hoist them itself:

@@ -303,6 +303,67 @@ __global__ void k_fill_sell(const int *__restrict__ ptr, const int *__restrict__
   }
 }
 
+// Column window of each kRingRT-row group (spmv_ring_op): [min, max] column
+// of its nonzeros, and its own rows when a split diagonal gathers x[row].
+__global__ void k_win_range(const int *__restrict__ ptr, const int *__restrict__ idx, int rows, bool own,
+                            int2 *win) {
+  const int r0 = blockIdx.x * kRingRT, r1 = min(rows, r0 + kRingRT);
+  int lo = own ? r0 : INT_MAX, hi = own ? r1 - 1 : -1;
+  for (int k = ptr[r0] + (int)threadIdx.x, e = ptr[r1]; k < e; k += blockDim.x) {
+    const int c = idx[k];
+    lo = min(lo, c);
+    hi = max(hi, c);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ int slo[32], shi[32];
+  if ((threadIdx.x & 31) == 0) {
+    slo[threadIdx.x >> 5] = lo;
+    shi[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      lo = min(lo, slo[w]);
+      hi = max(hi, shi[w]);
+    }
+    win[blockIdx.x] = make_int2(lo, hi);
+  }
+}
+
+// Plan the ring path of M into `win` (device, win_groups(M) entries): true
+// when every group's window, and the next group's new columns, fit the ring.
+static int win_groups(const DevCsr &M) { return (M.rows + kRingRT - 1) / kRingRT; }
+static int plan_ring(aqp_ctx *ctx, DevCsr &M, int2 *win, bool &ok) {
+  ok = false;
+  const int ng = win_groups(M);
+  if (ng < 2 * ctx->sm_count) return AQP_OK;  // a strip per SM needs a few groups
+  cudaStream_t st = ctx->stream;
+  k_win_range<<<ng, 256, 0, st>>>(M.ptr, M.idx, M.rows, M.diag != nullptr, win);
+  AQP_CUDA(cudaGetLastError());
+  std::vector<int2> h(ng);
+  AQP_CUDA(cudaMemcpyAsync(h.data(), win, (size_t)ng * sizeof(int2), cudaMemcpyDeviceToHost, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  // monotone windows: prefix maximum of the upper ends, suffix minimum of
+  // the lower ends (a group may then only ever need columns the ring adds
+  // in order); an empty window sits just above its upper end
+  for (int g = 1; g < ng; ++g) h[g].y = std::max(h[g].y, h[g - 1].y);
+  for (int g = ng - 2; g >= 0; --g) h[g].x = std::min(h[g].x, h[g + 1].x);
+  for (int g = 0; g < ng; ++g)
+    if (h[g].x > h[g].y) h[g].x = h[g].y + 1;
+  for (int g = 0; g + 1 < ng; ++g) {
+    if ((int64_t)h[g + 1].y - h[g].x >= kRingS) return AQP_OK;   // window + next columns exceed the ring
+    if ((int64_t)h[g + 1].y - h[g].y > 2 * kRingRT) return AQP_OK;  // two new columns per thread and group
+  }
+  AQP_CUDA(cudaMemcpyAsync(win, h.data(), (size_t)ng * sizeof(int2), cudaMemcpyHostToDevice, st));
+  AQP_CUDA(cudaStreamSynchronize(st));
+  ok = true;
+  return AQP_OK;
+}
+
 // The SELL-32 arrays live in a caller-provided buffer (aqp_problem_attach_sell),
 // the offsets in the problem's persistent workspace: dropping them frees nothing.
 void free_sell(DevCsr &M, cudaStream_t st) {
@@ -310,6 +371,9 @@ void free_sell(DevCsr &M, cudaStream_t st) {
   M.sell_off = nullptr;
   M.sell_idx = nullptr;
   M.sell_val = nullptr;
+  M.win = nullptr;
+  M.win_groups = 0;
+  M.win_grid = 0;
   M.sell_perm = nullptr;
 }
 
@@ -1158,12 +1222,20 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
 }
 
 static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+// the banded ring path (AQP_RING=0 turns it off) for unsharded problems
+static bool ring_on(const aqp_problem *p) {
+  const char *e = getenv("AQP_RING");
+  return p->nranks == 1 && !(e && e[0] == '0');
+}
 
 int aqp_problem_sell_bytes(const aqp_problem *p, size_t *bytes) {
   if (!p || !bytes) return fail(AQP_EINVAL, "NULL argument");
   size_t b = 0;
   for (int i = 0; i < 5; ++i)
     if (p->sell_total[i]) b += align256((size_t)p->sell_total[i] * 4) + align256((size_t)p->sell_total[i] * 8);
+  if (ring_on(p))  // ring windows of A and A' (Q's passes stay on the tile kernels: RingOf)
+    for (int i = 0; i < 2; ++i)
+      if (p->sell_total[i]) b += align256((size_t)win_groups(i == 0 ? p->A : p->At) * sizeof(int2));
   *bytes = b;
   return AQP_OK;
 }
@@ -1203,6 +1275,24 @@ int aqp_problem_attach_sell(aqp_problem *p, void *buf, size_t bytes) {
     M.sell_off = stores[i]->sell_off;
     M.sell_idx = sidx;
     M.sell_val = sval;
+  }
+  p->info.ring_mask = 0;
+  if (ring_on(p)) {
+    for (int i = 0; i < 2; ++i) {
+      DevCsr &M = *mats[i];
+      if (!p->sell_total[i]) continue;
+      int2 *win = reinterpret_cast<int2 *>(at);
+      at += align256((size_t)win_groups(M) * sizeof(int2));
+      if (!M.sell_idx || !(M.uniform || M.sell_perm) || M.row_off) continue;
+      bool ok = false;
+      AQP_TRY(plan_ring(p->ctx, M, win, ok));
+      if (ok) {
+        p->info.ring_mask |= 1 << i;
+        M.win = win;
+        M.win_groups = win_groups(M);
+        M.win_grid = std::min(p->ctx->sm_count, M.win_groups);
+      }
+    }
   }
   AQP_CUDA(cudaStreamSynchronize(st));
   p->info.a_items = p->A.nitems;

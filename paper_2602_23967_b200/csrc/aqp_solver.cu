@@ -187,6 +187,7 @@ struct OpP1Bb {
   static constexpr int NS = 0, NM = 0;
   static constexpr bool SYM = false, FINAL = false;
   static constexpr bool ROWIN_LATE = true;
+  static constexpr bool RING = false;  // measured slower on the ring (aqp_kernels.cuh RingOf)
   static constexpr int UNIFORM_BLOCKS = AQP_P1_BLOCKS;
   SV v;
   const double *y;
@@ -265,6 +266,7 @@ struct OpGrad {
   static constexpr int NS = INIT ? 4 : 7, NM = 0;
   static constexpr bool SYM = true, FINAL = true, SPLIT = true;
   static constexpr bool ROWIN_LATE = true;   // see aqp_kernels.cuh RowInLateOf
+  static constexpr bool RING = false;        // measured slower on the ring (aqp_kernels.cuh RingOf)
   static constexpr int UNIFORM_BLOCKS = AQP_GRAD_BLOCKS;
   SV v;
   const double *xt, *cen, *xo, *go;
@@ -1497,8 +1499,44 @@ cudaError_t add_node(cudaGraph_t g, GNode &last, unsigned grid, K fn, A... args)
   return add_node_smem(g, last, grid, 0u, fn, args...);
 }
 
+// banded ring path (spmv_ring_op): M.win is set when M's band fits the ring
+template <class Op>
+cudaError_t ring_attr() {
+  cudaError_t e = cudaFuncSetAttribute(spmv_ring_op<Op, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kRingS * 8);
+  if constexpr (!Op::SYM)
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(spmv_ring_op<Op, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingS * 8);
+  return e;
+}
+template <class Op>
+cudaError_t node_ring(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
+  cudaError_t e = ring_attr<Op>();
+  if (e != cudaSuccess) return e;
+  if constexpr (!Op::SYM)
+    if (M.sell_perm)
+      return add_node_cfg(g, last, (unsigned)M.win_grid, (unsigned)kRingRT, (unsigned)(kRingS * 8),
+                          spmv_ring_op<Op, true>, M, op, gr);
+  return add_node_cfg(g, last, (unsigned)M.win_grid, (unsigned)kRingRT, (unsigned)(kRingS * 8),
+                      spmv_ring_op<Op, false>, M, op, gr);
+}
+template <class Op>
+cudaError_t run_ring(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
+  cudaError_t e = ring_attr<Op>();
+  if (e != cudaSuccess) return e;
+  if constexpr (!Op::SYM)
+    if (M.sell_perm) {
+      spmv_ring_op<Op, true><<<M.win_grid, kRingRT, kRingS * 8, st>>>(M, op, gr);
+      return cudaGetLastError();
+    }
+  spmv_ring_op<Op, false><<<M.win_grid, kRingRT, kRingS * 8, st>>>(M, op, gr);
+  return cudaGetLastError();
+}
+
 template <class Op>
 cudaError_t node_spmv(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
+  if constexpr (kRingable<Op>)
+    if (M.win) return node_ring(g, last, M, op, gr);
   if (M.sell_perm) return add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_sellp_op<Op>, M, op, gr);
   if (M.uniform) return add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_op<Op, true>, M, op, gr);
   return add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M, op, gr);
@@ -1528,7 +1566,8 @@ void run_fold(cudaStream_t st, const Op &op, GridRed gr, unsigned nb) {
 // SPLIT ops: the main launch followed by its one-block fold/finalize
 template <class Op>
 cudaError_t node_spmv_fin(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
-  cudaError_t e = M.sell_perm ? add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_sellp_op<Op>, M, op, gr)
+  cudaError_t e = (kRingable<Op> && M.win) ? node_ring(g, last, M, op, gr)
+                  : M.sell_perm ? add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_sellp_op<Op>, M, op, gr)
                    : M.uniform  ? add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_op<Op, true>, M, op, gr)
                                 : add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M,
                                                 op, gr);
@@ -1558,6 +1597,8 @@ cudaError_t node_barrier(cudaGraph_t g, GNode &last, GridRed gr) {
 
 template <class Op>
 cudaError_t run_spmv(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
+  if constexpr (kRingable<Op>)
+    if (M.win) return run_ring(st, M, op, gr);
   if (M.sell_perm)
     spmv_sellp_op<Op><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
   else if (M.uniform)
@@ -1573,7 +1614,10 @@ cudaError_t run_elem(cudaStream_t st, int64_t n, const Op &op, GridRed gr) {
 }
 template <class Op>
 cudaError_t run_spmv_fin(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
-  if (M.sell_perm)
+  if (kRingable<Op> && M.win) {
+    cudaError_t e = run_ring(st, M, op, gr);
+    if (e != cudaSuccess) return e;
+  } else if (M.sell_perm)
     spmv_sellp_op<Op><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
   else if (M.uniform)
     spmv_op<Op, true><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
