@@ -173,8 +173,8 @@ typedef struct {
   int64_t a_items, at_items, q_items;   /* SpMV work items (blocks) per pass */
   int32_t quad_kind, r_dense;
   size_t persistent_bytes;
-  int32_t ring_mask;  /* bit 0 / 1: A / A' passes may use the banded ring
-                         kernel (set by aqp_problem_attach_sell) */
+  int32_t ring_mask;  /* bit 0 / 1 / 2: A / A' / Q passes may use the banded
+                         ring kernel (set by aqp_problem_attach_sell) */
 } aqp_problem_info;
 
 typedef struct aqp_problem aqp_problem;

@@ -43,9 +43,12 @@ constexpr int kTileNnz = 2048;         // nonzeros staged per SpMV row-block (16
 constexpr int kSegNnz = 8192;          // nonzeros per block for a split long row
 constexpr int kThreadRowMax = 48;      // longest row handled one-thread-per-row
 constexpr int kMaxRed = 16;            // max reduction slots of one kernel
-constexpr int kRingRT = 1024;          // ring path: rows per group (kRingRT / kThreads tiles)
-constexpr int kRingSub = kRingRT / kThreads;
-constexpr int kRingS = 16384;          // ring path: cached columns of the gathered vector (128 KB)
+// ring path (spmv_ring_op): rows per group = threads per CTA, and the ring of
+// cached columns of the gathered vector -- 1024 rows / 16384 columns (128 KB,
+// one CTA per SM) or 512 rows / 12288 columns (96 KB, two CTAs per SM)
+constexpr int kRingRT = 1024, kRingS = 16384;
+constexpr int kRingRT2 = 512, kRingS2 = 12288;
+__host__ __device__ constexpr int ring_cols(int rt) { return rt == kRingRT2 ? kRingS2 : kRingS; }
 
 // ---------------------------------------------------------------- scalar helpers
 // Reference semantics: _clip in _core.pyx:21-26 (lo first, then hi; NaN passes through)
@@ -461,7 +464,8 @@ struct DevCsr {
   // minimum, y: prefix maximum); null when the band does not fit the ring
   const int2 *win = nullptr;
   int win_groups = 0;
-  int win_grid = 0;  // persistent grid: one 1024-thread CTA per SM
+  int win_rt = 0;    // rows per group (kRingRT or kRingRT2)
+  int win_grid = 0;  // persistent grid: the CTAs resident at once
 };
 
 }  // namespace aqp

@@ -571,8 +571,8 @@ __global__ void __launch_bounds__(kThreads, UniformBlocksOf<Op>::value) spmv_sel
 // SpMV passes over banded matrices (C5's A, A', Q: every row's columns lie
 // within +-w of the row) gather from a ring of the source vector held in
 // shared memory instead of from L2.  One 1024-thread CTA per SM walks a
-// contiguous strip of row groups (kRingRT rows = kRingSub tiles of 256); per
-// group it adds the ~kRingRT columns the band newly reaches (DevCsr::win, read
+// contiguous strip of row groups (RT rows = RT / 256 tiles); per
+// group it adds the ~RT columns the band newly reaches (DevCsr::win, read
 // from HBM once per strip) while the group's rows gather their products from
 // the ring -- random 8-byte L2 sector reads become shared-memory loads, and the
 // matrix stream has the memory system to itself.  Each 256-thread sub-block
@@ -631,11 +631,19 @@ __device__ __forceinline__ void sub_reduce(RedVals<NS, NM> &v, double *smem, int
   sub_sync(sub);
 }
 
-// the op with its gather served from the ring
-template <class Op>
+// the op with its gather served from the ring of S columns
+template <class Op, int S>
 struct RingOp : Op {
   const double *ring_;
-  __device__ __forceinline__ double gather(int c) const { return ring_[c & (kRingS - 1)]; }
+  __device__ __forceinline__ double gather(int c) const { return ring_[(unsigned)c % S]; }
+};
+
+#ifndef AQP_RING_ROWIN_EARLY  // 1: ring rows load their epilogue operands before the row sum
+#define AQP_RING_ROWIN_EARLY 1   // (C5, every op on the ring: P2 1.865 -> 1.781 ms, P1 2.429 -> 2.325)
+#endif
+template <class O>
+struct RingLate {
+  static constexpr bool value = RowInLateOf<O>::value && !AQP_RING_ROWIN_EARLY;
 };
 
 // row r of a natural SELL-32 matrix (spmv_item's THREAD path on SELL storage)
@@ -644,7 +652,7 @@ __device__ __forceinline__ void ring_sell_row(const DevCsr &M, const O &o, int r
   if (r >= M.rows) return;
   using RowIn = typename RowInOf<O>::type;
   RowIn rin{};
-  if constexpr (RowInOf<O>::value && !RowInLateOf<O>::value) rin = o.load_row(r);
+  if constexpr (RowInOf<O>::value && !RingLate<O>::value) rin = o.load_row(r);
   const int b = __ldg(M.ptr + r), e = __ldg(M.ptr + r + 1);
   const int rg = r + M.row_off;
   double lo = 0.0, up = 0.0;
@@ -686,7 +694,7 @@ __device__ __forceinline__ void ring_sell_row(const DevCsr &M, const O &o, int r
     }
   }
   const double val = O::SYM ? lo + up : up;
-  if constexpr (RowInOf<O>::value && RowInLateOf<O>::value) rin = o.load_row(r);
+  if constexpr (RowInOf<O>::value && RingLate<O>::value) rin = o.load_row(r);
   if constexpr (RowInOf<O>::value) o.row_in(r, val, rin, acc); else o.row(r, val, acc);
 }
 
@@ -701,7 +709,7 @@ __device__ __forceinline__ void ring_sellp_tile(const DevCsr &M, const O &o, int
   using RowIn = typename RowInOf<O>::type;
   RowIn rin{};
   const bool has = rn < M.rows;
-  if constexpr (RowInOf<O>::value && !RowInLateOf<O>::value)
+  if constexpr (RowInOf<O>::value && !RingLate<O>::value)
     if (has) rin = o.load_row(rn);
   const int r = has ? blk + (int)__ldg(M.sell_perm + rn) : blk;
   int b = 0, e = 0;
@@ -755,12 +763,14 @@ __device__ __forceinline__ void ring_sellp_tile(const DevCsr &M, const O &o, int
   sub_sync(sub);
   if (has) {
     const double val = ssum[t];
-    if constexpr (RowInOf<O>::value && RowInLateOf<O>::value) rin = o.load_row(rn);
+    if constexpr (RowInOf<O>::value && RingLate<O>::value) rin = o.load_row(rn);
     if constexpr (RowInOf<O>::value) o.row_in(rn, val, rin, acc); else o.row(rn, val, acc);
   }
 }
 
-// Op::RING = false keeps an op on the tile kernels.  Measured on C5 (bench
+// Op::RING_CLASS (1: the BB gradient, 2: A'y of P1, 0: every other op)
+// selects the ops AQP_RING_OFF (bit mask, default 0b110) keeps on the tile
+// kernels.  Measured on C5 (bench
 // kernel table, same box): the A x̄ pass P2 1.998 -> 1.863 ms and the power
 // iteration gain; the BB gradient (Q's +-1000 band already hits L1/L2, seven
 // epilogue streams) 1.17 -> 1.75 ms and A'y (P1, SELL-P with its per-tile
@@ -768,30 +778,31 @@ __device__ __forceinline__ void ring_sellp_tile(const DevCsr &M, const O &o, int
 // 1024-thread CTA per SM and a barrier per group the epilogue loads of a heavy
 // op are exposed, where 48 independent warps of the tile kernel hide them.
 template <class Op, class = void>
-struct RingOf {
-  static constexpr bool value = true;
+struct RingClassOf {
+  static constexpr int value = 0;
 };
 template <class Op>
-struct RingOf<Op, std::void_t<decltype(Op::RING)>> {
-  static constexpr bool value = Op::RING;
+struct RingClassOf<Op, std::void_t<decltype(Op::RING_CLASS)>> {
+  static constexpr int value = Op::RING_CLASS;
 };
 // ops the ring kernel serves: no reduction, or split reductions (partials
 // only -- the last-block ticket of cold ops stays with spmv_op)
 template <class Op>
-constexpr bool kRingable = (!Op::FINAL || SplitOf<Op>::value) && RingOf<Op>::value;
+constexpr bool kRingable = !Op::FINAL || SplitOf<Op>::value;
 
-template <class Op, bool SELLP>
-__global__ void __launch_bounds__(kRingRT, 1) spmv_ring_op(DevCsr M, Op op, GridRed g) {
+template <class Op, bool SELLP, int RT>
+__global__ void __launch_bounds__(RT, kRingRT / RT) spmv_ring_op(DevCsr M, Op op, GridRed g) {
   constexpr int NS = Op::NS, NM = Op::NM;
+  constexpr int kRingSub = RT / kThreads, S = ring_cols(RT);
   extern __shared__ double ring[];
   __shared__ double sred[kRingSub][kWarps * kMaxRed];
-  __shared__ double ssum[SELLP ? kRingRT : 1];
-  __shared__ int lrow[SELLP ? kRingRT : 1];
+  __shared__ double ssum[SELLP ? RT : 1];
+  __shared__ int lrow[SELLP ? RT : 1];
   __shared__ int nlr[kRingSub];
   pdl_wait();
   trace_mark(g, 0);
   if (op.skip()) return;
-  RingOp<Op> o;
+  RingOp<Op, S> o;
   static_cast<Op &>(o) = op;
   o.prepare();
   o.ring_ = ring;
@@ -802,16 +813,16 @@ __global__ void __launch_bounds__(kRingRT, 1) spmv_ring_op(DevCsr M, Op op, Grid
   const int g1 = (int)((int64_t)(blockIdx.x + 1) * ng / gridDim.x);
   if (g0 < g1) {
     const int2 w0 = M.win[g0];
-    for (int c = w0.x + t; c <= w0.y; c += kRingRT) ring[c & (kRingS - 1)] = src.gather(c);
+    for (int c = w0.x + t; c <= w0.y; c += RT) ring[(unsigned)c % S] = src.gather(c);
     int have = w0.y;
     __syncthreads();
     const unsigned nb = (unsigned)M.nitems;
     for (int gi = g0; gi < g1; ++gi) {
       // the next group's new columns: loaded now, stored after this group's
-      // rows (the plan guarantees win[g+1].y - win[g].x < kRingS, so they
-      // never overwrite a column this group still reads)
+      // rows (the plan guarantees win[g+1].y - win[g].x < S, so they never
+      // overwrite a column this group still reads)
       const int nh = gi + 1 < g1 ? M.win[gi + 1].y : have;
-      const int c0 = have + 1 + t, c1 = c0 + kRingRT;
+      const int c0 = have + 1 + t, c1 = c0 + RT;
       const double p0 = c0 <= nh ? src.gather(c0) : 0.0;
       const double p1 = c1 <= nh ? src.gather(c1) : 0.0;
       const int tile = gi * kRingSub + sub;
@@ -832,8 +843,8 @@ __global__ void __launch_bounds__(kRingRT, 1) spmv_ring_op(DevCsr M, Op op, Grid
           }
         }
       }
-      if (c0 <= nh) ring[c0 & (kRingS - 1)] = p0;
-      if (c1 <= nh) ring[c1 & (kRingS - 1)] = p1;
+      if (c0 <= nh) ring[(unsigned)c0 % S] = p0;
+      if (c1 <= nh) ring[(unsigned)c1 % S] = p1;
       have = nh;
       __syncthreads();
     }

@@ -303,11 +303,11 @@ __global__ void k_fill_sell(const int *__restrict__ ptr, const int *__restrict__
   }
 }
 
-// Column window of each kRingRT-row group (spmv_ring_op): [min, max] column
+// Column window of each rt-row group (spmv_ring_op): [min, max] column
 // of its nonzeros, and its own rows when a split diagonal gathers x[row].
-__global__ void k_win_range(const int *__restrict__ ptr, const int *__restrict__ idx, int rows, bool own,
+__global__ void k_win_range(const int *__restrict__ ptr, const int *__restrict__ idx, int rows, int rt, bool own,
                             int2 *win) {
-  const int r0 = blockIdx.x * kRingRT, r1 = min(rows, r0 + kRingRT);
+  const int r0 = blockIdx.x * rt, r1 = min(rows, r0 + rt);
   int lo = own ? r0 : INT_MAX, hi = own ? r1 - 1 : -1;
   for (int k = ptr[r0] + (int)threadIdx.x, e = ptr[r1]; k < e; k += blockDim.x) {
     const int c = idx[k];
@@ -336,13 +336,18 @@ __global__ void k_win_range(const int *__restrict__ ptr, const int *__restrict__
 
 // Plan the ring path of M into `win` (device, win_groups(M) entries): true
 // when every group's window, and the next group's new columns, fit the ring.
-static int win_groups(const DevCsr &M) { return (M.rows + kRingRT - 1) / kRingRT; }
+// rows per group: AQP_RING_RT=512 selects the two-CTAs-per-SM form
+static int ring_rt() {
+  const char *e = getenv("AQP_RING_RT");
+  return e && atoi(e) == kRingRT2 ? kRingRT2 : kRingRT;
+}
+static int win_groups(const DevCsr &M) { return (M.rows + ring_rt() - 1) / ring_rt(); }
 static int plan_ring(aqp_ctx *ctx, DevCsr &M, int2 *win, bool &ok) {
   ok = false;
-  const int ng = win_groups(M);
+  const int rt = ring_rt(), S = ring_cols(rt), ng = win_groups(M);
   if (ng < 2 * ctx->sm_count) return AQP_OK;  // a strip per SM needs a few groups
   cudaStream_t st = ctx->stream;
-  k_win_range<<<ng, 256, 0, st>>>(M.ptr, M.idx, M.rows, M.diag != nullptr, win);
+  k_win_range<<<ng, 256, 0, st>>>(M.ptr, M.idx, M.rows, rt, M.diag != nullptr, win);
   AQP_CUDA(cudaGetLastError());
   std::vector<int2> h(ng);
   AQP_CUDA(cudaMemcpyAsync(h.data(), win, (size_t)ng * sizeof(int2), cudaMemcpyDeviceToHost, st));
@@ -355,8 +360,8 @@ static int plan_ring(aqp_ctx *ctx, DevCsr &M, int2 *win, bool &ok) {
   for (int g = 0; g < ng; ++g)
     if (h[g].x > h[g].y) h[g].x = h[g].y + 1;
   for (int g = 0; g + 1 < ng; ++g) {
-    if ((int64_t)h[g + 1].y - h[g].x >= kRingS) return AQP_OK;   // window + next columns exceed the ring
-    if ((int64_t)h[g + 1].y - h[g].y > 2 * kRingRT) return AQP_OK;  // two new columns per thread and group
+    if ((int64_t)h[g + 1].y - h[g].x >= S) return AQP_OK;       // window + next columns exceed the ring
+    if ((int64_t)h[g + 1].y - h[g].y > 2 * rt) return AQP_OK;   // two new columns per thread and group
   }
   AQP_CUDA(cudaMemcpyAsync(win, h.data(), (size_t)ng * sizeof(int2), cudaMemcpyHostToDevice, st));
   AQP_CUDA(cudaStreamSynchronize(st));
@@ -373,6 +378,7 @@ void free_sell(DevCsr &M, cudaStream_t st) {
   M.sell_val = nullptr;
   M.win = nullptr;
   M.win_groups = 0;
+  M.win_rt = 0;
   M.win_grid = 0;
   M.sell_perm = nullptr;
 }
@@ -1233,9 +1239,9 @@ int aqp_problem_sell_bytes(const aqp_problem *p, size_t *bytes) {
   size_t b = 0;
   for (int i = 0; i < 5; ++i)
     if (p->sell_total[i]) b += align256((size_t)p->sell_total[i] * 4) + align256((size_t)p->sell_total[i] * 8);
-  if (ring_on(p))  // ring windows of A and A' (Q's passes stay on the tile kernels: RingOf)
-    for (int i = 0; i < 2; ++i)
-      if (p->sell_total[i]) b += align256((size_t)win_groups(i == 0 ? p->A : p->At) * sizeof(int2));
+  if (ring_on(p))  // ring windows of A, A' and Q (which ops use them: AQP_RING_OFF)
+    for (int i = 0; i < 3; ++i)
+      if (p->sell_total[i]) b += align256((size_t)win_groups(i == 0 ? p->A : i == 1 ? p->At : p->Q) * sizeof(int2));
   *bytes = b;
   return AQP_OK;
 }
@@ -1278,7 +1284,7 @@ int aqp_problem_attach_sell(aqp_problem *p, void *buf, size_t bytes) {
   }
   p->info.ring_mask = 0;
   if (ring_on(p)) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
       DevCsr &M = *mats[i];
       if (!p->sell_total[i]) continue;
       int2 *win = reinterpret_cast<int2 *>(at);
@@ -1290,7 +1296,8 @@ int aqp_problem_attach_sell(aqp_problem *p, void *buf, size_t bytes) {
         p->info.ring_mask |= 1 << i;
         M.win = win;
         M.win_groups = win_groups(M);
-        M.win_grid = std::min(p->ctx->sm_count, M.win_groups);
+        M.win_rt = ring_rt();
+        M.win_grid = std::min(p->ctx->sm_count * (kRingRT / M.win_rt), M.win_groups);
       }
     }
   }

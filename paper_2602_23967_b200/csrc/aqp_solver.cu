@@ -187,7 +187,7 @@ struct OpP1Bb {
   static constexpr int NS = 0, NM = 0;
   static constexpr bool SYM = false, FINAL = false;
   static constexpr bool ROWIN_LATE = true;
-  static constexpr bool RING = false;  // measured slower on the ring (aqp_kernels.cuh RingOf)
+  static constexpr int RING_CLASS = 2;  // AQP_RING_OFF bit 2 (aqp_kernels.cuh RingClassOf)
   static constexpr int UNIFORM_BLOCKS = AQP_P1_BLOCKS;
   SV v;
   const double *y;
@@ -266,7 +266,7 @@ struct OpGrad {
   static constexpr int NS = INIT ? 4 : 7, NM = 0;
   static constexpr bool SYM = true, FINAL = true, SPLIT = true;
   static constexpr bool ROWIN_LATE = true;   // see aqp_kernels.cuh RowInLateOf
-  static constexpr bool RING = false;        // measured slower on the ring (aqp_kernels.cuh RingOf)
+  static constexpr int RING_CLASS = 1;       // AQP_RING_OFF bit 1 (aqp_kernels.cuh RingClassOf)
   static constexpr int UNIFORM_BLOCKS = AQP_GRAD_BLOCKS;
   SV v;
   const double *xt, *cen, *xo, *go;
@@ -1499,44 +1499,64 @@ cudaError_t add_node(cudaGraph_t g, GNode &last, unsigned grid, K fn, A... args)
   return add_node_smem(g, last, grid, 0u, fn, args...);
 }
 
-// banded ring path (spmv_ring_op): M.win is set when M's band fits the ring
+// banded ring path (spmv_ring_op): M.win is set when M's band fits the ring;
+// AQP_RING_OFF (bit c: ops of RingClassOf c) keeps op classes on the tile
+// kernels -- default 0b110, the gradient and P1 (measured slower on the ring)
+static int ring_off_mask() {
+  const char *e = getenv("AQP_RING_OFF");  // read per graph build / eager launch (tests toggle it)
+  return e ? atoi(e) : 0b110;
+}
 template <class Op>
+bool use_ring(const DevCsr &M) {
+  if constexpr (!kRingable<Op>) return false;
+  return M.win && !((ring_off_mask() >> RingClassOf<Op>::value) & 1);
+}
+template <class Op, int RT>
 cudaError_t ring_attr() {
-  cudaError_t e = cudaFuncSetAttribute(spmv_ring_op<Op, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kRingS * 8);
+  const int smem = ring_cols(RT) * 8;
+  cudaError_t e = cudaFuncSetAttribute(spmv_ring_op<Op, false, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if constexpr (!Op::SYM)
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(spmv_ring_op<Op, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingS * 8);
+      e = cudaFuncSetAttribute(spmv_ring_op<Op, true, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   return e;
+}
+template <class Op, int RT>
+cudaError_t node_ring_rt(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
+  cudaError_t e = ring_attr<Op, RT>();
+  if (e != cudaSuccess) return e;
+  const unsigned smem = (unsigned)(ring_cols(RT) * 8);
+  if constexpr (!Op::SYM)
+    if (M.sell_perm)
+      return add_node_cfg(g, last, (unsigned)M.win_grid, (unsigned)RT, smem, spmv_ring_op<Op, true, RT>, M, op, gr);
+  return add_node_cfg(g, last, (unsigned)M.win_grid, (unsigned)RT, smem, spmv_ring_op<Op, false, RT>, M, op, gr);
 }
 template <class Op>
 cudaError_t node_ring(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
-  cudaError_t e = ring_attr<Op>();
+  return M.win_rt == kRingRT2 ? node_ring_rt<Op, kRingRT2>(g, last, M, op, gr)
+                              : node_ring_rt<Op, kRingRT>(g, last, M, op, gr);
+}
+template <class Op, int RT>
+cudaError_t run_ring_rt(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
+  cudaError_t e = ring_attr<Op, RT>();
   if (e != cudaSuccess) return e;
+  const int smem = ring_cols(RT) * 8;
   if constexpr (!Op::SYM)
-    if (M.sell_perm)
-      return add_node_cfg(g, last, (unsigned)M.win_grid, (unsigned)kRingRT, (unsigned)(kRingS * 8),
-                          spmv_ring_op<Op, true>, M, op, gr);
-  return add_node_cfg(g, last, (unsigned)M.win_grid, (unsigned)kRingRT, (unsigned)(kRingS * 8),
-                      spmv_ring_op<Op, false>, M, op, gr);
+    if (M.sell_perm) {
+      spmv_ring_op<Op, true, RT><<<M.win_grid, RT, smem, st>>>(M, op, gr);
+      return cudaGetLastError();
+    }
+  spmv_ring_op<Op, false, RT><<<M.win_grid, RT, smem, st>>>(M, op, gr);
+  return cudaGetLastError();
 }
 template <class Op>
 cudaError_t run_ring(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
-  cudaError_t e = ring_attr<Op>();
-  if (e != cudaSuccess) return e;
-  if constexpr (!Op::SYM)
-    if (M.sell_perm) {
-      spmv_ring_op<Op, true><<<M.win_grid, kRingRT, kRingS * 8, st>>>(M, op, gr);
-      return cudaGetLastError();
-    }
-  spmv_ring_op<Op, false><<<M.win_grid, kRingRT, kRingS * 8, st>>>(M, op, gr);
-  return cudaGetLastError();
+  return M.win_rt == kRingRT2 ? run_ring_rt<Op, kRingRT2>(st, M, op, gr) : run_ring_rt<Op, kRingRT>(st, M, op, gr);
 }
 
 template <class Op>
 cudaError_t node_spmv(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
   if constexpr (kRingable<Op>)
-    if (M.win) return node_ring(g, last, M, op, gr);
+    if (use_ring<Op>(M)) return node_ring(g, last, M, op, gr);
   if (M.sell_perm) return add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_sellp_op<Op>, M, op, gr);
   if (M.uniform) return add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_op<Op, true>, M, op, gr);
   return add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M, op, gr);
@@ -1566,7 +1586,7 @@ void run_fold(cudaStream_t st, const Op &op, GridRed gr, unsigned nb) {
 // SPLIT ops: the main launch followed by its one-block fold/finalize
 template <class Op>
 cudaError_t node_spmv_fin(cudaGraph_t g, GNode &last, const DevCsr &M, const Op &op, GridRed gr) {
-  cudaError_t e = (kRingable<Op> && M.win) ? node_ring(g, last, M, op, gr)
+  cudaError_t e = use_ring<Op>(M) ? node_ring(g, last, M, op, gr)
                   : M.sell_perm ? add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_sellp_op<Op>, M, op, gr)
                    : M.uniform  ? add_node_smem(g, last, (unsigned)M.nitems, 0u, spmv_op<Op, true>, M, op, gr)
                                 : add_node_smem(g, last, (unsigned)M.nitems, (unsigned)M.smem_bytes, spmv_op<Op>, M,
@@ -1598,7 +1618,7 @@ cudaError_t node_barrier(cudaGraph_t g, GNode &last, GridRed gr) {
 template <class Op>
 cudaError_t run_spmv(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
   if constexpr (kRingable<Op>)
-    if (M.win) return run_ring(st, M, op, gr);
+    if (use_ring<Op>(M)) return run_ring(st, M, op, gr);
   if (M.sell_perm)
     spmv_sellp_op<Op><<<M.nitems, kThreads, 0, st>>>(M, op, gr);
   else if (M.uniform)
@@ -1614,7 +1634,7 @@ cudaError_t run_elem(cudaStream_t st, int64_t n, const Op &op, GridRed gr) {
 }
 template <class Op>
 cudaError_t run_spmv_fin(cudaStream_t st, const DevCsr &M, const Op &op, GridRed gr) {
-  if (kRingable<Op> && M.win) {
+  if (use_ring<Op>(M)) {
     cudaError_t e = run_ring(st, M, op, gr);
     if (e != cudaSuccess) return e;
   } else if (M.sell_perm)

@@ -24,16 +24,22 @@ def _ring_mask(problem):
     return DeviceProblem(problem, DeviceContext.get(0)).info.ring_mask
 
 
-def _solve(problem, ring: bool, **kw):
-    old = os.environ.get("AQP_RING")
-    os.environ["AQP_RING"] = "1" if ring else "0"
+KNOBS = ("AQP_RING", "AQP_RING_OFF", "AQP_RING_RT")
+
+
+def _solve(problem, ring, **kw):
+    """ring: False (AQP_RING=0: tile kernels only), True (default policy) or
+    a dict of ring knobs (AQP_RING_OFF op mask, AQP_RING_RT group size)."""
+    env = {"AQP_RING": "0"} if ring is False else ({} if ring is True else dict(ring))
+    saved = {k: os.environ.pop(k, None) for k in KNOBS}
+    os.environ.update(env)
     try:
         return aq.solve(problem, aq.SolverParams(eps_tol=1e-8, **kw))
     finally:
-        if old is None:
-            del os.environ["AQP_RING"]
-        else:
-            os.environ["AQP_RING"] = old
+        for k in KNOBS:
+            os.environ.pop(k, None)
+            if saved[k] is not None:
+                os.environ[k] = saved[k]
 
 
 def _same(r1, r2):
@@ -43,28 +49,37 @@ def _same(r1, r2):
     assert r1.report.kkt_max == r2.report.kkt_max
 
 
+# default policy; every op on the ring (gradient and P1 too); the same with
+# 512-row groups and two CTAs per SM
+POLICIES = [True, {"AQP_RING_OFF": "0"}, {"AQP_RING_OFF": "0", "AQP_RING_RT": "512"}]
+
+
 @pytest.mark.parametrize("n,w", [(400_000, 2000), (1_000_000, 5000)])
 def test_ring_solve_bitwise_equals_tile_kernels(cuda, n, w):
     p = generators.banded_qp(n, n, half_width=w, seed=3)
     os.environ.pop("AQP_RING", None)
-    assert _ring_mask(p) == 0b11  # A (SELL pairs) and A' (SELL-P) windows planned
-    _same(_solve(p, True, iter_limit=40), _solve(p, False, iter_limit=40))
+    assert _ring_mask(p) == 0b111  # A (SELL pairs), A' (SELL-P) and Q (plain SELL) windows planned
+    want = _solve(p, False, iter_limit=40)
+    for pol in POLICIES:
+        _same(_solve(p, pol, iter_limit=40), want)
 
 
 def test_ring_solve_to_optimal_matches(cuda):
     # a whole solve (restarts, certification, the norm estimate) through the ring
     p = generators.banded_qp(400_000, 400_000, half_width=300, seed=1)
-    r1, r2 = _solve(p, True), _solve(p, False)
-    assert r1.status == aq.SolveStatus.OPTIMAL
-    _same(r1, r2)
+    want = _solve(p, False)
+    assert want.status == aq.SolveStatus.OPTIMAL
+    for pol in POLICIES:
+        _same(_solve(p, pol), want)
 
 
 def test_ring_off_when_band_exceeds_ring(cuda):
     # A's +-9000 columns: a 1024-row group's window (~19k columns) exceeds
-    # the 16384-entry ring -> A and A' run the tile kernels, same result
+    # the 16384-entry ring -> A and A' run the tile kernels (Q's +-1000 band
+    # still fits), same result
     p = generators.banded_qp(400_000, 400_000, half_width=9000, seed=2)
     os.environ.pop("AQP_RING", None)
-    assert _ring_mask(p) == 0
+    assert _ring_mask(p) == 0b100
     _same(_solve(p, True, iter_limit=10), _solve(p, False, iter_limit=10))
 
 
