@@ -381,7 +381,7 @@ def run_ours(args, world, rank, local):
                                                               "x_post", "bb_fold"))
     top = kernels["bb_gradient"]
     traffic = None  # ncu dram__bytes_{read,write}.sum of the same kernel (scripts/profile_r02.sh)
-    for prof in ("ncu_summary_r02.json", "ncu_summary.json"):
+    for prof in ("ncu_summary_r02e.json", "ncu_summary_r02.json", "ncu_summary.json"):
         try:
             traffic = json.load(open(os.path.join(ROOT, "profiles", prof)))["kernels"]["c5_bb_gradient"][
                 "dram_bytes_per_launch"]
