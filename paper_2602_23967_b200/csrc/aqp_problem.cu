@@ -176,9 +176,15 @@ __global__ void k_iota(int *out, int64_t n) {
     out[i] = (int)i;
 }
 
-__global__ void k_hist(const int *__restrict__ keys, int64_t n, int *counts) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(counts + keys[i], 1);  // integer counts: order-independent
+// Key counts from the SORTED keys (counts zeroed): a run [i, j] of key k adds
+// j + 1 - i, as two atomics at its ends -- two per distinct key instead of one
+// per entry (C5's A': 1e8 instead of 5e8 scattered atomics, 21 -> ~2 ms)
+__global__ void k_run_counts(const int *__restrict__ s, int64_t n, int *counts) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = s[i];
+    if (i == 0 || s[i - 1] != k) atomicSub(counts + k, (int)i);
+    if (i == n - 1 || s[i + 1] != k) atomicAdd(counts + k, (int)(i + 1));
+  }
 }
 
 // transpose keys restricted to the column window [col0, col1): an entry
@@ -689,12 +695,13 @@ int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool 
     }
     k_row_ids<<<setup_grid(src.rows), 256, 0, st>>>(src.ptr, src.rows, rid);
     k_iota<<<setup_grid(nnz), 256, 0, st>>>(vals, nnz);
-    k_hist<<<setup_grid(nnz), 256, 0, st>>>(sort_keys, nnz, counts);  // counts[rows_t]: outside the window
     AQP_CUDA(cudaGetLastError());
     int end_bit = 1;
     while ((1LL << end_bit) <= (int64_t)rows_t) ++end_bit;
     size_t need = tb;
     AQP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, sort_keys, keys2, vals, vals2, (int)nnz, 0, end_bit, st));
+    k_run_counts<<<setup_grid(nnz), 256, 0, st>>>(keys2, nnz, counts);  // counts[rows_t]: outside the window
+    AQP_CUDA(cudaGetLastError());
     if (window) {
       int outside = 0;
       AQP_CUDA(cudaMemcpyAsync(&outside, counts + rows_t, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -746,13 +753,14 @@ int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool s
     k_row_ids<<<setup_grid(U.rows), 256, 0, st>>>(U.ptr, U.rows, rid);
     k_sym_keys<<<setup_grid(nnz), 256, 0, st>>>(rid, U.idx, nnz, (int)row_base, (int)r0, (int)r1, keys);
     k_iota<<<setup_grid(n2), 256, 0, st>>>(vals, n2);
-    k_hist<<<setup_grid(n2), 256, 0, st>>>(keys, n2, counts);  // counts[n] = #sentinels (diagonal mirrors, outside)
     AQP_CUDA(cudaGetLastError());
     int end_bit = 1;
     while ((1LL << end_bit) <= (int64_t)n) ++end_bit;
     size_t need = tb;
     step_mark(st, "  symmetrize.keys");
     AQP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, keys, keys2, vals, vals2, (int)n2, 0, end_bit, st));
+    k_run_counts<<<setup_grid(n2), 256, 0, st>>>(keys2, n2, counts);  // counts[n] = #sentinels (diagonal mirrors, outside)
+    AQP_CUDA(cudaGetLastError());
     step_mark(st, "  symmetrize.sort");
     int ndiag = 0;
     AQP_CUDA(cudaMemcpyAsync(&ndiag, counts + n, sizeof(int), cudaMemcpyDeviceToHost, st));

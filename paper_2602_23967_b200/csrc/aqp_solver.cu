@@ -1162,6 +1162,7 @@ template <bool RED>
 struct OpPwA {  // tm = A v  (|A v|^2 -> red[slot] when RED)
   static constexpr int NS = RED ? 1 : 0, NM = 0;
   static constexpr bool SYM = false, FINAL = RED;
+  static constexpr int RING_CLASS = 4;  // AQP_RING_OFF bit 4
   SV v;
   int slot;
   const double *x;
@@ -1185,6 +1186,7 @@ struct OpPwA {  // tm = A v  (|A v|^2 -> red[slot] when RED)
 struct OpPwAt {  // w = A' tm -> xbb[dst], |w|^2; the fold sets the next v (or stops)
   static constexpr int NS = 1, NM = 0;
   static constexpr bool SYM = false, FINAL = true, SPLIT = true;
+  static constexpr int RING_CLASS = 3;  // AQP_RING_OFF bit 3
   SV v;
   int dst;
   double *w;
@@ -1500,8 +1502,9 @@ cudaError_t add_node(cudaGraph_t g, GNode &last, unsigned grid, K fn, A... args)
 }
 
 // banded ring path (spmv_ring_op): M.win is set when M's band fits the ring;
-// AQP_RING_OFF (bit c: ops of RingClassOf c) keeps op classes on the tile
-// kernels -- default 0b110, the gradient and P1 (measured slower on the ring)
+// AQP_RING_OFF (bit c: ops of RingClassOf c -- 1 gradient, 2 P1, 3 / 4 the
+// power iteration's A'w / A v, 0 every other op) keeps op classes on the
+// tile kernels -- default 0b110, the gradient and P1 (measured slower on the ring)
 static int ring_off_mask() {
   const char *e = getenv("AQP_RING_OFF");  // read per graph build / eager launch (tests toggle it)
   return e ? atoi(e) : 0b110;
