@@ -37,7 +37,9 @@ int upload_csr(aqp_ctx *ctx, CsrStore &s, DevCsr &M, int64_t rows, int64_t cols,
                const int64_t *d_idx, const double *d_val, int64_t nnz, const int64_t *host_ptr, bool strict,
                int *d_bad);
 int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool strict, Bump &scratch,
-                  int64_t col0 = 0, int64_t col1 = -1, int64_t row_base = 0, int64_t out_cols = -1);
+                  int64_t col0 = 0, int64_t col1 = -1, int64_t row_base = 0, int64_t out_cols = -1,
+                  bool *deferred = nullptr);
+int plan_deferred_at(aqp_problem *p);
 int symmetrize_csr(aqp_ctx *ctx, const DevCsr &U, CsrStore &f, DevCsr &F, bool strict, Bump &scratch,
                    int64_t *nfull_out, int64_t row_base = 0, int64_t r0 = 0, int64_t r1 = -1);
 size_t transpose_scratch_bytes(int64_t nnz, int64_t cols);
@@ -72,6 +74,10 @@ struct aqp_problem {
   int64_t q_full_nnz = 0;
   int64_t sell_total[5] = {};  // padded SELL-32 entries of A, A', Q, R, R' (0: no SELL copy)
   bool sell_sorted[5] = {};    // ... in the SELL-P (block-sorted) layout
+  // A' planned lazily: a staged (non-uniform) A' that gets the SELL-P layout
+  // never runs its CSR plan, so the host planning pass (0.12 s on C5's 5e7
+  // rows) waits until a solver needs it without SELL-P (plan_deferred_at)
+  bool at_plan_deferred = false;
   int r_dense = 0;  // R held dense row-major in R.val (R.rows x n); no R' CSR
   double *qdiag = nullptr;  // Q's diagonal when split out of its CSR (DevCsr::diag)
   double *c = nullptr, *vlo = nullptr, *vhi = nullptr, *qd = nullptr, *clo = nullptr, *chi = nullptr;

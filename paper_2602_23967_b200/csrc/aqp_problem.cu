@@ -624,6 +624,20 @@ int finish_plan(aqp_ctx *ctx, DevCsr &M, const int *host_ptr32, const int64_t *h
   return AQP_OK;
 }
 
+// The CSR plan of a deferred A' (see aqp_problem::at_plan_deferred): run when
+// a solver is created without the SELL-P copy attached (or SELL-P was not
+// chosen); the SELL-P attach replaces the plan by its own (one block per 256
+// rows), so the planning pass is skipped altogether on the common path.
+int plan_deferred_at(aqp_problem *p) {
+  if (!p->at_plan_deferred) return AQP_OK;
+  CsrStore &t = p->sAt;
+  AQP_TRY(finish_plan(p->ctx, p->At, nullptr, nullptr, false, t.plan, t.plan_cap, t.seg_part, t.seg_ticket,
+                      t.seg_cap, true));
+  p->at_plan_deferred = false;
+  p->info.at_items = p->At.nitems;
+  return AQP_OK;
+}
+
 // Persistent storage of one device CSR with its plan.
 void layout_csr(Bump &b, CsrStore &s, int64_t rows, int64_t nnz) {
   s.ptr = (int *)b.take((rows + 1) * sizeof(int));
@@ -668,7 +682,7 @@ int upload_csr(aqp_ctx *ctx, CsrStore &s, DevCsr &M, int64_t rows, int64_t cols,
 // the output's column count (default: src.rows).
 // Scratch: rid(nnz) keys(nnz) keys2(nnz) vals(nnz) vals2(nnz) counts(rows_t+1) + cub.
 int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool strict, Bump &scratch, int64_t col0,
-                  int64_t col1, int64_t row_base, int64_t out_cols) {
+                  int64_t col1, int64_t row_base, int64_t out_cols, bool *deferred) {
   cudaStream_t st = ctx->stream;
   const int64_t nnz = src.nnz;
   if (col1 < 0) col1 = src.cols;
@@ -721,6 +735,25 @@ int transpose_csr(aqp_ctx *ctx, const DevCsr &src, CsrStore &t, DevCsr &T, bool 
   T.ptr = t.ptr;
   T.idx = t.idx;
   T.val = t.val;
+  if (deferred) {
+    // a staged A' (mean row >= the staging threshold: its plan is never
+    // uniform, so SELL planning does not depend on it) waits for
+    // plan_deferred_at; everything else is planned now
+    double staged_min = 8.0;
+    if (const char *e = getenv("AQP_STAGED_MIN")) staged_min = atof(e);
+    *deferred = !strict && T.rows > 0 && (double)T.nnz >= staged_min * (double)T.rows;
+    if (*deferred) {
+      free_sell(T, st);
+      T.plan = nullptr;
+      T.nitems = 0;
+      T.uniform = 0;
+      T.smem_bytes = 0;
+      T.nlongseg = 0;
+      T.seg_part = t.seg_part;
+      T.seg_ticket = t.seg_ticket;
+      return AQP_OK;
+    }
+  }
   return finish_plan(ctx, T, nullptr, nullptr, strict, t.plan, t.plan_cap, t.seg_part, t.seg_ticket, t.seg_cap,
                      true);
 }
@@ -1124,7 +1157,7 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
                     false, p->bad);
     if (rc) return cleanup(rc);
     tm("A_convert_plan");
-    rc = transpose_csr(ctx, p->A, p->sAt, p->At, false, sc);
+    rc = transpose_csr(ctx, p->A, p->sAt, p->At, false, sc, 0, -1, 0, -1, &p->at_plan_deferred);
     tm("At_transpose_plan");
   } else {
     rc = shard_a(ctx, p, d, host_a_indptr, scratch, scratch_bytes);
@@ -1215,6 +1248,10 @@ int aqp_problem_create(aqp_ctx *ctx, const aqp_problem_desc *d, const int64_t *h
       if (rc) return cleanup(rc);
     }
   }
+  if (p->at_plan_deferred && !p->sell_sorted[1]) {  // no SELL-P for A': its CSR plan serves
+    rc = plan_deferred_at(p);
+    if (rc) return cleanup(rc);
+  }
   int bad = 0;
   AQP_CUDA(cudaMemcpyAsync(&bad, p->bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   AQP_CUDA(cudaStreamSynchronize(st));
@@ -1281,6 +1318,7 @@ int aqp_problem_attach_sell(aqp_problem *p, void *buf, size_t bytes) {
       M.uniform = 1;
       M.nitems = (M.rows + kThreads - 1) / kThreads;
       M.smem_bytes = 0;
+      if (i == 1) p->at_plan_deferred = false;  // the SELL-P plan replaces the CSR plan
     } else {
       k_fill_sell<<<(M.rows + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, M.val, M.rows, stores[i]->sell_off, sidx,
                                                         sval, i != 2);

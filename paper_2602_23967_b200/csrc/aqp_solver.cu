@@ -1942,6 +1942,9 @@ static int run_eager(aqp_solver *s, int64_t n_iters);
 
 int aqp_solver_sizes(const aqp_problem *p, size_t *workspace_bytes) {
   if (!p || !workspace_bytes) return fail(AQP_EINVAL, "NULL argument");
+  // the workspace is sized by the plans: a deferred A' plan is made now (the
+  // lazily computed part of the problem's state)
+  AQP_TRY(plan_deferred_at(const_cast<aqp_problem *>(p)));
   Bump b;
   SV v{};
   Ctrl *c = nullptr;
@@ -1953,6 +1956,7 @@ int aqp_solver_sizes(const aqp_problem *p, size_t *workspace_bytes) {
 
 int aqp_solver_create(aqp_problem *p, const aqp_solver_params *prm, void *ws, size_t ws_bytes, aqp_solver **out) {
   if (!p || !prm || !ws || !out) return fail(AQP_EINVAL, "NULL argument");
+  AQP_TRY(plan_deferred_at(p));  // A' without its SELL-P copy attached: the CSR plan now
   aqp_solver *s = new aqp_solver();
   s->p = p;
   s->prm = *prm;

@@ -179,7 +179,9 @@ class DeviceProblem:
         sell = C.c_size_t()
         nat.check(lib.aqp_problem_sell_bytes(h, C.byref(sell)), "aqp_problem_sell_bytes")
         self.sell = None
-        if sell.value:
+        # AQP_NO_SELL_ATTACH=1 (test hook): leave the SELL copies unattached, as
+        # a C-ABI caller may -- the CSR plans (incl. a deferred A' plan) serve
+        if sell.value and os.environ.get("AQP_NO_SELL_ATTACH", "") != "1":
             self.sell = self.ctx.empty(sell.value)
             nat.check(lib.aqp_problem_attach_sell(h, C.c_void_p(self.sell.data_ptr()), sell.value),
                       "aqp_problem_attach_sell")

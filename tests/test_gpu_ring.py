@@ -24,7 +24,7 @@ def _ring_mask(problem):
     return DeviceProblem(problem, DeviceContext.get(0)).info.ring_mask
 
 
-KNOBS = ("AQP_RING", "AQP_RING_OFF", "AQP_RING_RT")
+KNOBS = ("AQP_RING", "AQP_RING_OFF", "AQP_RING_RT", "AQP_NO_SELL_ATTACH", "AQP_SELL")
 
 
 def _solve(problem, ring, **kw):
@@ -88,3 +88,16 @@ def test_ring_off_for_small_problems(cuda):
     p = generators.banded_qp(100_000, 100_000, half_width=500, seed=0)
     os.environ.pop("AQP_RING", None)
     assert _ring_mask(p) == 0
+
+
+def test_unattached_sell_plans_deferred_at(cuda):
+    # C5's A' (mean row 10 >= the staging threshold) defers its CSR plan to the
+    # SELL-P attach; without the attach the solver plans it when created, and
+    # the solve is bitwise the one planned at problem creation (no SELL at all).
+    # (Not bitwise the SELL-P solve: A'-pass reductions -- the power
+    # iteration's |A'w|^2 -- fold per plan item, and the CSR plan's STAGED
+    # items are not the SELL-P plan's 256-row tiles.)
+    p = generators.banded_qp(400_000, 400_000, half_width=2000, seed=4)
+    want = _solve(p, {"AQP_SELL": "0"}, iter_limit=30)
+    got = _solve(p, {"AQP_NO_SELL_ATTACH": "1"}, iter_limit=30)
+    _same(got, want)
