@@ -302,11 +302,38 @@ class DeviceSolver:
     def reset_window(self):
         nat.check(self.lib.aqp_solver_reset_window(self.handle))
 
+    def _length(self, which: int) -> int:
+        n0, n1, m0, m1 = self.prob.rows
+        return m1 - m0 if which in (self.Y, self.YRAY0, self.YRAY1) else n1 - n0
+
+    def prefault(self, whiches) -> None:
+        """Allocate and page in the host buffers of coming reads (the result
+        vectors) on a background thread while the solve loop runs on the
+        device: a fresh 400 MB numpy array otherwise takes its page faults
+        inside the timed read-back."""
+        import threading
+
+        spare = {}
+
+        def work():
+            for w in whiches:
+                a = np.empty(self._length(w), dtype=np.float64)
+                a[::512] = 0.0  # one write per 4 KB page
+                spare[w] = a
+
+        self._spare = spare
+        self._prefault = threading.Thread(target=work, daemon=True)
+        self._prefault.start()
+
     def read(self, which: int) -> np.ndarray:
         """The whole vector, or (row shard) this rank's slice of it."""
-        n0, n1, m0, m1 = self.prob.rows
-        length = m1 - m0 if which in (self.Y, self.YRAY0, self.YRAY1) else n1 - n0
-        out = np.empty(length, dtype=np.float64)
+        length = self._length(which)
+        out = None
+        pf = getattr(self, "_prefault", None)
+        if pf is not None and not pf.is_alive():  # never wait for it
+            out = self._spare.pop(which, None)
+        if out is None:
+            out = np.empty(length, dtype=np.float64)
         nat.check(self.lib.aqp_solver_read(self.handle, int(which), out.ctypes.data, length), "aqp_solver_read")
         return out
 

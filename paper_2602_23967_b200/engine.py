@@ -418,6 +418,8 @@ def solve(problem, params: Optional[SolverParams] = None, progress: Optional[Pro
     sc = nat.Scalars()
     sc.eta, sc.omega, sc.theta, sc.inner_tol = rs.eta, rs.omega, rs.theta, tol0
     sol.init(sc)
+    # host buffers of the result vectors, paged in while the loop runs
+    run.checker.prefault((DeviceSolver.X_EVAL, DeviceSolver.Y, DeviceSolver.DUAL_SLACK))
 
     n_outer = n_inner = restarts = 0
 
