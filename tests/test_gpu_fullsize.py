@@ -6,7 +6,8 @@
   the Cython order: A x, A'y through the explicit transpose, the symmetric Q x);
 * the device setup scalars equal the host (numpy) values bitwise;
 * two solves of the same instance are bitwise identical (deterministic
-  reductions at full size).
+  reductions at full size);
+* the banded ring path gives bitwise the tile kernels' solve.
 """
 
 import numpy as np
@@ -57,3 +58,28 @@ def test_solve_deterministic_full_c5(cuda, c5):
     assert (r1.outer_iterations, r1.inner_iterations) == (r2.outer_iterations, r2.inner_iterations)
     assert np.array_equal(r1.x, r2.x) and np.array_equal(r1.y, r2.y)
     assert r1.report.kkt_max == r2.report.kkt_max
+
+
+def test_ring_path_bitwise_tile_kernels_full_c5(cuda, c5):
+    # the banded ring path (spmv_ring_op: P2 and the power iteration by
+    # default, every op with AQP_RING_OFF=0) against the tile kernels only
+    # (AQP_RING=0), at the full size: iterates, counts and KKT bit for bit
+    import os
+
+    prm = aq.SolverParams(eps_tol=1e-8, iter_limit=3)
+    runs = []
+    for env in ({"AQP_RING": "0"}, {}, {"AQP_RING_OFF": "0"}):
+        saved = {k: os.environ.pop(k, None) for k in ("AQP_RING", "AQP_RING_OFF")}
+        os.environ.update(env)
+        try:
+            runs.append(aq.solve(c5, prm))
+        finally:
+            for k, v in saved.items():
+                os.environ.pop(k, None)
+                if v is not None:
+                    os.environ[k] = v
+    want = runs[0]
+    for r in runs[1:]:
+        assert (r.outer_iterations, r.inner_iterations) == (want.outer_iterations, want.inner_iterations)
+        assert np.array_equal(r.x, want.x) and np.array_equal(r.y, want.y)
+        assert r.report.kkt_max == want.report.kkt_max
