@@ -453,6 +453,10 @@ struct DevCsr {
   // a shared-memory hand-off.  (Sorting within a warp only -- no block
   // barrier, natural slice widths -- measured slower: C5 A' 2.80 ms.)
   const uint8_t *sell_perm = nullptr;
+  // SELL-P: the length of the row at each sorted position (255: longer), so a
+  // thread starts its slice loads after one round trip instead of three
+  // (position -> row -> row pointers)
+  const uint8_t *sell_len = nullptr;
   // full symmetric Q of a uniform plan: its diagonal moved out of the CSR into
   // diag[local row].  A row's upper sum starts with diag * x[row] -- the
   // diagonal is the first j >= i entry, so the order is unchanged -- and the

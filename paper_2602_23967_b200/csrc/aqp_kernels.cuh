@@ -459,12 +459,7 @@ __device__ __forceinline__ void spmv_sellp_block(const DevCsr &M, const Op &o, R
   if constexpr (RowInOf<Op>::value && !RowInLateOf<Op>::value)
     if (has) rin = o.load_row(rn);
   const int r = has ? blk + (int)__ldg(M.sell_perm + rn) : blk;
-  int b = 0, e = 0;
-  if (has) {
-    b = __ldg(M.ptr + r);
-    e = __ldg(M.ptr + r + 1);
-  }
-  const int len = e - b;
+  const int len = has ? (int)__ldg(M.sell_len + rn) : 0;  // not behind the permutation load
   const bool lng = has && len > kThreadRowMax;
   if (t == 0) nlr = 0;
   if (has && !lng) {
@@ -712,12 +707,7 @@ __device__ __forceinline__ void ring_sellp_tile(const DevCsr &M, const O &o, int
   if constexpr (RowInOf<O>::value && !RingLate<O>::value)
     if (has) rin = o.load_row(rn);
   const int r = has ? blk + (int)__ldg(M.sell_perm + rn) : blk;
-  int b = 0, e = 0;
-  if (has) {
-    b = __ldg(M.ptr + r);
-    e = __ldg(M.ptr + r + 1);
-  }
-  const int len = e - b;
+  const int len = has ? (int)__ldg(M.sell_len + rn) : 0;  // not behind the permutation load
   const bool lng = has && len > kThreadRowMax;
   if (t == 0) *nlr = 0;
   if (has && !lng) {

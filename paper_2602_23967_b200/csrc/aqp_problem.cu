@@ -382,6 +382,7 @@ void free_sell(DevCsr &M, cudaStream_t st) {
   M.sell_off = nullptr;
   M.sell_idx = nullptr;
   M.sell_val = nullptr;
+  M.sell_len = nullptr;
   M.win = nullptr;
   M.win_groups = 0;
   M.win_rt = 0;
@@ -481,11 +482,12 @@ static int plan_sell(aqp_ctx *ctx, const DevCsr &M, int64_t *off, uint8_t *perm,
 
 __global__ void k_fill_sellp(const int *__restrict__ ptr, const int *__restrict__ idx, const double *__restrict__ val,
                              int rows, const uint8_t *__restrict__ perm, const int64_t *__restrict__ off, int *sidx,
-                             double *sval, bool pair) {
+                             double *sval, bool pair, uint8_t *lens) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= rows) return;
   const int64_t r = (p & ~(int64_t)255) + perm[p];
   const int b = ptr[r], e = ptr[r + 1];
+  lens[p] = (uint8_t)min(e - b, 255);  // DevCsr::sell_len (> kThreadRowMax: a long row)
   if (e - b > kThreadRowMax) return;  // long rows stay in the CSR
   const int64_t off0 = off[p >> 5];
   const int lane = (int)(p & 31);
@@ -1283,7 +1285,10 @@ int aqp_problem_sell_bytes(const aqp_problem *p, size_t *bytes) {
   if (!p || !bytes) return fail(AQP_EINVAL, "NULL argument");
   size_t b = 0;
   for (int i = 0; i < 5; ++i)
-    if (p->sell_total[i]) b += align256((size_t)p->sell_total[i] * 4) + align256((size_t)p->sell_total[i] * 8);
+    if (p->sell_total[i]) {
+      b += align256((size_t)p->sell_total[i] * 4) + align256((size_t)p->sell_total[i] * 8);
+      if (p->sell_sorted[i]) b += align256((size_t)(i == 0 ? p->A : i == 1 ? p->At : i == 2 ? p->Q : i == 3 ? p->R : p->Rt).rows);
+    }
   if (ring_on(p))  // ring windows of A, A' and Q (which ops use them: AQP_RING_OFF)
     for (int i = 0; i < 3; ++i)
       if (p->sell_total[i]) b += align256((size_t)win_groups(i == 0 ? p->A : i == 1 ? p->At : p->Q) * sizeof(int2));
@@ -1311,8 +1316,11 @@ int aqp_problem_attach_sell(aqp_problem *p, void *buf, size_t bytes) {
     double *sval = reinterpret_cast<double *>(at);
     at += align256((size_t)tot * 8);
     if (p->sell_sorted[i]) {
+      uint8_t *lens = reinterpret_cast<uint8_t *>(at);
+      at += align256((size_t)M.rows);
       k_fill_sellp<<<(M.rows + 255) / 256, 256, 0, st>>>(M.ptr, M.idx, M.val, M.rows, stores[i]->sell_perm,
-                                                         stores[i]->sell_off, sidx, sval, i != 2);
+                                                         stores[i]->sell_off, sidx, sval, i != 2, lens);
+      M.sell_len = lens;
       // the SELL-P kernel runs one block per 256 rows and sums long rows itself
       M.sell_perm = stores[i]->sell_perm;
       M.uniform = 1;
